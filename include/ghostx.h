@@ -1,0 +1,168 @@
+/*
+ * ghostx.h — C ABI of the B200-native ghost-cell exchange library
+ * (libghostx.so, built from paper_2403_12179_b200/csrc/).
+ *
+ * It replaces the hot path of the reference package miniamr_core
+ * (/root/reference/pkg/src/miniamr_core/comm.py):
+ *
+ *   plan builder   _shift_candidates / _build_copy_segments / CommPlan /
+ *                  plan_build_fill_boundary / parallel_copy plan part
+ *                  (comm.py:250-309, :413-424)        -> ghx_plan_build_*
+ *   executor       _execute_plan (local fused copy, pack, Bus send/recv,
+ *                  unpack; comm.py:316-380)            -> ghx_exec_*
+ *   BoxArray ctor  O(n^2) disjointness check (mesh.py:203-205)
+ *                                                       -> ghx_boxes_disjoint
+ *
+ * Conventions (all plain C types, no torch types):
+ *  - a box is six int64: lo0 lo1 lo2 hi0 hi1 hi2, padded to 3 axes with
+ *    lo = hi = 0 on unused axes (core/mesh.py:31-40);
+ *  - fab storage is F-order (nx, ny, nz, ncomp) over the fab's storage
+ *    (grown) box, element size 4 or 8 bytes, copied as raw words;
+ *  - every function returns GHX_OK (0) or a GHX_E* code and never throws;
+ *    ghx_last_error() returns a thread-local message for the last failure;
+ *  - plans are immutable after build and may be shared by threads; an exec
+ *    handle is owned by one rank (thread or process) at a time;
+ *  - device calls are stream-ordered on the cudaStream_t passed as void*.
+ */
+#ifndef GHOSTX_H
+#define GHOSTX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GHX_OK 0
+#define GHX_EINVAL 1
+#define GHX_ECUDA 2
+#define GHX_ENOMEM 3
+#define GHX_EOVERLAP 4
+
+#define GHX_MODE_FILL_BOUNDARY 0
+#define GHX_MODE_PARALLEL_COPY 1
+
+/* executor kinds (ghx_exec_create) */
+#define GHX_EXEC_DIRECT 0 /* local tags + remote tags pushed into peer fabs   */
+#define GHX_EXEC_LOCAL 1  /* only tags whose src and dst rank are this rank   */
+#define GHX_EXEC_PACK 2   /* remote tags of this rank -> per-peer send buffer */
+#define GHX_EXEC_UNPACK 3 /* per-peer recv buffer -> remote tags into my fabs */
+
+typedef struct ghx_plan ghx_plan;
+typedef struct ghx_exec ghx_exec;
+
+const char *ghx_last_error(void);
+int ghx_version(void);
+
+/* ------------------------------------------------------------ box algebra */
+
+/* Replaces the O(n^2) pairwise check in BoxArray.__init__ (mesh.py:203-205)
+ * with a binned sweep.  *overlap_a = *overlap_b = -1 when disjoint, else the
+ * lexicographically first overlapping pair (a < b). */
+int ghx_boxes_disjoint(int64_t nboxes, const int64_t *boxes, int64_t *overlap_a,
+                       int64_t *overlap_b);
+
+/* ------------------------------------------------------------------ plans */
+
+/* plan_build_fill_boundary (comm.py:289-309) minus the Python-side cache and
+ * validation: dst targets = grow(box, ngrow), sources = valid boxes, the
+ * (si == dj, shift == 0) pair excluded, pieces cut by box_diff against the
+ * dst valid box (index_space.py:297-320); segments sorted by
+ * (dst_fab, dst_lo, src_fab, shift) and grouped by (src_rank, dst_rank)
+ * like CommPlan (comm.py:218-237).  periodic[d] != 0 marks periodic axes,
+ * period[d] = geom.period (domain cell extent, index_space.py:371-374). */
+int ghx_plan_build_fill_boundary(int64_t nboxes, const int64_t *boxes, const int64_t ngrow[3],
+                                 const int32_t periodic[3], const int64_t period[3],
+                                 const int32_t *rank_of, int32_t nranks, ghx_plan **out);
+
+/* parallel_copy plan (comm.py:413-424): dst targets grow(dst_box, ngrow_dst),
+ * sources grow(src_box, ngrow_src); periodic == NULL means geom=None (only
+ * the zero shift, comm.py:253-254). */
+int ghx_plan_build_parallel_copy(int64_t ndst, const int64_t *dst_boxes, const int64_t ngrow_dst[3],
+                                 int64_t nsrc, const int64_t *src_boxes, const int64_t ngrow_src[3],
+                                 const int32_t *periodic, const int64_t period[3],
+                                 const int32_t *src_rank, const int32_t *dst_rank, int32_t nranks,
+                                 ghx_plan **out);
+
+void ghx_plan_free(ghx_plan *plan);
+int64_t ghx_plan_num_segments(const ghx_plan *plan);
+/* rows of 13 int64: src_fab dst_fab dlo0 dlo1 dlo2 dhi0 dhi1 dhi2 s0 s1 s2
+ * src_rank dst_rank, in CommPlan sort order (src box = dst box - shift). */
+int ghx_plan_get_segments(const ghx_plan *plan, int64_t *rows);
+/* number of write tags after last-writer-wins clipping (== segments unless
+ * destinations overlap: nodal data or ngrow_src > 0). */
+int64_t ghx_plan_num_write_tags(const ghx_plan *plan);
+/* per (src_rank, dst_rank) cell totals of the reference segments:
+ * out[(s * nranks + d)] = cells (local pairs s == d included). */
+int ghx_plan_pair_cells(const ghx_plan *plan, int64_t *out);
+
+/* ------------------------------------------------------------- executors */
+
+/* Compile the plan for one rank and one storage layout into a device tag
+ * table (one fused launch per run).  src_fab_boxes / dst_fab_boxes: storage
+ * (grown) box of every src / dst fab (nsrc*6, ndst*6), ncomp_total the
+ * fab's component count; components [scomp, scomp+ncomp) of src land in
+ * [dcomp, dcomp+ncomp) of dst.  elem_bytes: 4 or 8. */
+int ghx_exec_create(const ghx_plan *plan, int32_t rank, int32_t kind, const int64_t *src_fab_boxes,
+                    int32_t src_ncomp_total, const int64_t *dst_fab_boxes, int32_t dst_ncomp_total,
+                    int32_t scomp, int32_t dcomp, int32_t ncomp, int32_t elem_bytes, int32_t device,
+                    ghx_exec **out);
+void ghx_exec_free(ghx_exec *ex);
+
+/* Run the fused copy kernel.  ptrs: device-accessible base pointers, laid
+ * out as [nsrc src fabs][ndst dst fabs][nranks send buffers][nranks recv
+ * buffers]; entries never referenced by this rank's tags may be NULL.
+ * Base pointers must be 16-byte aligned. */
+int ghx_exec_run(ghx_exec *ex, void *const *ptrs, int64_t nptrs, void *stream);
+
+/* Introspection: tags, warp tasks, elements moved per run, algorithmic
+ * bytes (read + write) per run, per-peer buffer elements (out[nranks]). */
+int ghx_exec_info(const ghx_exec *ex, int64_t *ntags, int64_t *ntasks, int64_t *elems,
+                  int64_t *alg_bytes);
+int ghx_exec_buffer_elems(const ghx_exec *ex, int64_t *per_peer);
+
+/* Launch-time tuning knob (warps per block * blocks): 0 = default. */
+int ghx_exec_set_grid(ghx_exec *ex, int32_t blocks, int32_t threads);
+
+/* -------------------------------------------------------------- devices */
+
+int ghx_device_alloc(int32_t device, size_t bytes, void **out);
+int ghx_device_free(void *ptr);
+int ghx_host_alloc(size_t bytes, void **out); /* pinned + mapped */
+int ghx_host_free(void *ptr);
+int ghx_memset_u64(void *ptr, uint64_t value, size_t count, void *stream);
+int ghx_enable_peer_access(int32_t device, int32_t peer);
+int ghx_ipc_get_handle(void *ptr, uint8_t handle[64]);
+int ghx_ipc_open_handle(int32_t device, const uint8_t handle[64], void **out);
+int ghx_ipc_close_handle(void *ptr);
+int ghx_stream_sync(void *stream);
+
+/* Cross-rank device barrier: rank writes `epoch` into flags[p][rank] of
+ * every peer p (system-scope release), then spins until its own
+ * flags[rank][p] >= epoch for all p (acquire).  flag_ptrs[p] is rank p's
+ * flag array (nranks uint64) as mapped in this process. */
+int ghx_signal_barrier(uint64_t *const *flag_ptrs, int32_t rank, int32_t nranks, uint64_t epoch,
+                       void *stream);
+
+/* Synthetic input generator (bench / tests): valid cells of the fab get
+ * splitmix64(seed ^ lin(i,j,k,c)) mapped to [0,1) (see oracle/inputs.py),
+ * every other storage cell gets the signalling-NaN poison. */
+int ghx_fill_hash(void *fab, const int64_t fab_box[6], int32_t ncomp, const int64_t valid_box[6],
+                  const int64_t domain_box[6], uint64_t seed, int32_t elem_bytes, void *stream);
+
+/* Expected state after a FillBoundary of a field filled by ghx_fill_hash:
+ * every storage cell whose periodically wrapped coordinate lies in the
+ * domain holds the hash of the wrapped cell, every other cell the poison.
+ * (Size-independent parity property for full-size configurations.) */
+int ghx_fill_hash_wrapped(void *fab, const int64_t fab_box[6], int32_t ncomp, const int64_t domain_box[6],
+                          const int32_t periodic[3], uint64_t seed, int32_t elem_bytes, void *stream);
+
+/* Number of fused-copy kernel launches issued by this process. */
+int64_t ghx_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GHOSTX_H */

@@ -79,10 +79,12 @@ def shift_ranges(src, tgt, periodic, period):
     n = src.shape[0]
     kmin = np.zeros((n, 3), np.int64)
     kmax = np.zeros((n, 3), np.int64)
-    if periodic is None:
-        return kmin, kmax
     for d in range(3):
-        if not periodic[d]:
+        if periodic is None or not periodic[d]:
+            # only k = 0; mark the axis empty when the boxes cannot meet (the
+            # reference finds the same pairs through its intersect() test)
+            miss = (src[:, d] > tgt[3 + d]) | (src[:, 3 + d] < tgt[d])
+            kmin[miss, d] = 1
             continue
         p = int(period[d])
         # ceil((t.lo - s.hi)/p) and floor((t.hi - s.lo)/p), exact integer math

@@ -1,0 +1,829 @@
+"""FillBoundary / ParallelCopy: cached plans, one fused launch per call.
+
+Drop-in for the hot path of the reference's ``miniamr_core.comm``
+(/root/reference/pkg/src/miniamr_core/comm.py):
+
+====================================  =========================================
+reference (comm.py)                   here
+====================================  =========================================
+Bus / RankContext / runtime_spawn     same semantics (ranks are threads, one
+  :35-180                             per GPU round-robin); plus a process
+                                      context when torch.distributed is up
+PlanKey / CopySegment / CommPlan      same fields; segments come from the
+  :189-247                            native binned builder (ghx_plan_*)
+plan_build_fill_boundary :289-309     same validation order, per-MultiFab
+                                      cache and ``plan_builds`` counter
+_execute_plan :316-380                ghx_exec_run: ONE fused sm_100a launch
+                                      moves local tags and pushes remote tags
+                                      straight into the peer's fabs
+                                      (NCCL send/recv only as a fallback)
+fill_boundary :383-394                same contract, synchronous
+parallel_copy :397-429                same contract, synchronous
+====================================  =========================================
+
+Message accounting keeps the reference's contract (tests/test_comm.py:182,
+:236, :356): per call at most one "message" per ordered rank pair, bytes =
+cells * ncomp * itemsize of the reference segments for that pair.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import itertools
+import os
+import threading
+import weakref
+from collections import deque
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from . import config
+from .index_space import Box, Geometry, IntVect
+from .mesh import MultiFab, Slab
+
+SUM, MIN, MAX = "sum", "min", "max"
+_COMBINE = {SUM: lambda a, b: a + b, MIN: min, MAX: max}
+
+
+class RankFailure(RuntimeError):
+    def __init__(self, rank: int, cause: BaseException):
+        super().__init__(f"rank {rank} failed: {cause!r}")
+        self.rank = rank
+        self.cause = cause
+
+
+# --------------------------------------------------------------- rank runtime
+
+class Bus:
+    """In-process transport shared by thread ranks: FIFO per ordered pair,
+    exactly-once delivery, per-pair [messages, bytes] statistics."""
+
+    def __init__(self, nranks: int):
+        self.nranks = nranks
+        self._cond = threading.Condition()
+        self._queues = {(s, d): deque() for s in range(nranks) for d in range(nranks)}
+        self.message_stats = {(s, d): [0, 0] for s in range(nranks) for d in range(nranks)}
+        self.barrier = threading.Barrier(nranks) if nranks > 1 else None
+        self._slots: list = [None] * nranks
+        self._failed: int | None = None
+
+    def _count(self, src: int, dst: int, nbytes: int) -> None:
+        st = self.message_stats[(src, dst)]
+        st[0] += 1
+        st[1] += int(nbytes)
+
+    def send(self, src: int, dst: int, payload, nbytes: int) -> None:
+        with self._cond:
+            self._queues[(src, dst)].append(payload)
+            self._count(src, dst, nbytes)
+            self._cond.notify_all()
+
+    def account(self, src: int, dst: int, nbytes: int) -> None:
+        """Record one message whose bytes moved device-to-device (the
+        fused kernel stored them straight into the receiver's fabs)."""
+        with self._cond:
+            self._count(src, dst, nbytes)
+
+    def recv(self, src: int, dst: int):
+        with self._cond:
+            q = self._queues[(src, dst)]
+            while not q:
+                if self._failed is not None:
+                    raise RuntimeError(f"recv aborted: rank {self._failed} failed")
+                self._cond.wait(timeout=0.1)
+            return q.popleft()
+
+    def fail(self, rank: int) -> None:
+        with self._cond:
+            if self._failed is None:
+                self._failed = rank
+            self._cond.notify_all()
+        if self.barrier is not None:
+            self.barrier.abort()
+
+    def stats_snapshot(self) -> dict:
+        with self._cond:
+            return {k: tuple(v) for k, v in self.message_stats.items()}
+
+    def format_stats(self) -> str:
+        rows = [f"  {s}->{d}: {n} messages, {b} bytes"
+                for (s, d), (n, b) in sorted(self.stats_snapshot().items()) if n]
+        return "\n".join(["comm message stats (src->dst: messages, bytes):"] + (rows or ["  (no messages)"]))
+
+
+def _cuda_devices() -> int:
+    try:
+        import torch
+        return torch.cuda.device_count() if torch.cuda.is_available() else 0
+    except Exception:
+        return 0
+
+
+class RankContext:
+    """Per-rank handle: rank id, device, shared bus."""
+
+    kind = "thread"
+
+    def __init__(self, rank: int, nranks: int, bus: Bus, device: int | None = None):
+        self.rank = rank
+        self.nranks = nranks
+        self.bus = bus
+        self._device = device
+
+    @property
+    def device(self) -> int:
+        if self._device is not None:
+            return self._device
+        if _cuda_devices():
+            import torch
+            return torch.cuda.current_device()
+        return 0
+
+    def send(self, dst: int, payload, nbytes: int = 0) -> None:
+        self.bus.send(self.rank, dst, payload, nbytes)
+
+    def recv(self, src: int):
+        return self.bus.recv(src, self.rank)
+
+    def barrier(self) -> None:
+        if self.bus.barrier is not None:
+            self.bus.barrier.wait()
+
+    def allgather(self, obj) -> list:
+        if self.nranks == 1:
+            return [obj]
+        self.bus._slots[self.rank] = obj
+        self.barrier()
+        out = list(self.bus._slots)
+        self.barrier()
+        return out
+
+    def allreduce(self, ops, values) -> tuple:
+        ops = tuple(ops)
+        values = tuple(float(v) for v in values)
+        if len(ops) != len(values):
+            raise ValueError("allreduce needs one value per op")
+        if self.nranks == 1:
+            return values
+        slots = self.allgather((ops, values))
+        if any(s[0] != ops for s in slots):
+            raise ValueError("mismatched reduction op lists across ranks")
+        out = list(slots[0][1])
+        for _, vals in slots[1:]:
+            out = [_COMBINE[op](a, b) for op, a, b in zip(ops, out, vals)]
+        return tuple(out)
+
+
+class ProcessContext:
+    """One process per GPU under torch.distributed (torchrun): rank = the
+    process group rank, device = LOCAL_RANK.  Bus statistics record the
+    messages this process sends."""
+
+    kind = "process"
+
+    def __init__(self):
+        import torch
+        import torch.distributed as dist
+        self._dist = dist
+        self.rank = dist.get_rank()
+        self.nranks = dist.get_world_size()
+        self.bus = Bus(self.nranks) if self.nranks == 1 else _LocalBus(self.nranks)
+        ndev = _cuda_devices()
+        local = int(os.environ.get("LOCAL_RANK", self.rank))
+        self.device = (local % ndev) if ndev else 0
+        self.backend = dist.get_backend()
+
+    def barrier(self) -> None:
+        if self.nranks > 1:
+            self._dist.barrier()
+
+    def allgather(self, obj) -> list:
+        if self.nranks == 1:
+            return [obj]
+        out = [None] * self.nranks
+        self._dist.all_gather_object(out, obj)
+        return out
+
+    def allreduce(self, ops, values) -> tuple:
+        ops = tuple(ops)
+        values = tuple(float(v) for v in values)
+        slots = self.allgather((ops, values))
+        if any(s[0] != ops for s in slots):
+            raise ValueError("mismatched reduction op lists across ranks")
+        out = list(slots[0][1])
+        for _, vals in slots[1:]:
+            out = [_COMBINE[op](a, b) for op, a, b in zip(ops, out, vals)]
+        return tuple(out)
+
+    def send(self, dst, payload, nbytes=0):
+        raise NotImplementedError("object send/recv is only available between thread ranks")
+
+    recv = send
+
+
+class _LocalBus(Bus):
+    def __init__(self, nranks):
+        super().__init__(1)
+        self.nranks = nranks
+        self.message_stats = {(s, d): [0, 0] for s in range(nranks) for d in range(nranks)}
+        self.barrier = None
+
+
+_tls = threading.local()
+_serial_ctx = RankContext(0, 1, Bus(1))
+_process_ctx: ProcessContext | None = None
+
+
+def current_ctx():
+    ctx = getattr(_tls, "ctx", None)
+    if ctx is not None:
+        return ctx
+    global _process_ctx
+    try:
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized():
+            if _process_ctx is None or _process_ctx.nranks != dist.get_world_size():
+                _process_ctx = ProcessContext()
+            return _process_ctx
+    except Exception:
+        pass
+    return _serial_ctx
+
+
+def current_rank() -> int:
+    return current_ctx().rank
+
+
+def runtime_spawn(nranks: int, program) -> list:
+    """Run program(ctx) once per logical rank on its own thread; rank r
+    drives GPU r % device_count.  A raising rank aborts the run and surfaces
+    as RankFailure with the root-cause rank (reference comm.py:143-180)."""
+    if nranks < 1:
+        raise ValueError("nranks must be >= 1")
+    bus = Bus(nranks)
+    ndev = _cuda_devices()
+
+    def dev_of(r):
+        return (r % ndev) if ndev else 0
+
+    if nranks == 1:
+        prev = getattr(_tls, "ctx", None)
+        _tls.ctx = RankContext(0, 1, bus, dev_of(0))
+        try:
+            return [program(_tls.ctx)]
+        finally:
+            _tls.ctx = prev
+    results: list = [None] * nranks
+    failures: dict = {}
+
+    def main(r: int) -> None:
+        _tls.ctx = RankContext(r, nranks, bus, dev_of(r))
+        try:
+            if ndev:
+                import torch
+                torch.cuda.set_device(dev_of(r))
+            results[r] = program(_tls.ctx)
+        except BaseException as exc:  # noqa: BLE001 - propagate with rank id
+            failures[r] = exc
+            bus.fail(r)
+        finally:
+            _tls.ctx = None
+
+    threads = [threading.Thread(target=main, args=(r,), name=f"rank{r}") for r in range(nranks)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if failures:
+        r = bus._failed if bus._failed in failures else min(failures)
+        raise RankFailure(r, failures[r]) from failures[r]
+    return results
+
+
+def global_reduce(ops, values, ctx=None) -> tuple:
+    ctx = ctx or current_ctx()
+    return ctx.allreduce(ops, values)
+
+
+# ---------------------------------------------------------------------- plans
+
+@dataclass(frozen=True)
+class PlanKey:
+    src_ba: int
+    src_dm: int
+    dst_ba: int
+    dst_dm: int
+    ngrow_src: tuple
+    ngrow_dst: tuple
+    ixtype: tuple
+    periodic: tuple
+    op: str
+
+
+@dataclass(frozen=True)
+class CopySegment:
+    src_fab: int
+    dst_fab: int
+    src_box: Box
+    dst_box: Box
+    shift: tuple
+
+    @property
+    def cells(self) -> int:
+        return self.dst_box.num_pts
+
+
+_plan_uid = itertools.count(1)
+_plan_lock = threading.Lock()
+# process-wide cache of native plans so per-rank MultiFabs sharing a layout
+# build once; per-MultiFab ``plan_cache`` / ``plan_builds`` still follow the
+# reference exactly
+_global_plans: "weakref.WeakValueDictionary" = weakref.WeakValueDictionary()
+
+
+class CommPlan:
+    """Cached copy schedule: sorted segments grouped into per-rank local
+    lists and per-ordered-pair message lists (comm.py:218-247)."""
+
+    def __init__(self, handle: int, nranks: int, dim: int, ixtype):
+        self.uid = next(_plan_uid)
+        self._h = C.c_void_p(handle)
+        self.nranks = nranks
+        self._dim = dim
+        self._ixtype = ixtype
+        self.num_segments = int(N.lib.ghx_plan_num_segments(self._h))
+        self.num_write_tags = int(N.lib.ghx_plan_num_write_tags(self._h))
+        pc = np.zeros(nranks * nranks, np.int64)
+        N.check(N.lib.ghx_plan_pair_cells(self._h, N.i64p(pc)))
+        self.pair_cells = pc.reshape(nranks, nranks)
+        self._rows = None
+        self._groups = None
+        self._execs: dict = {}
+        self._lock = threading.Lock()
+
+    @property
+    def is_empty(self) -> bool:
+        return self.num_segments == 0
+
+    def rows(self) -> np.ndarray:
+        """(num_segments, 13) int64: src dst dlo(3) dhi(3) shift(3) srank drank."""
+        if self._rows is None:
+            r = np.zeros((self.num_segments, 13), np.int64)
+            if self.num_segments:
+                N.check(N.lib.ghx_plan_get_segments(self._h, N.i64p(r)))
+            self._rows = r
+        return self._rows
+
+    def _build_groups(self):
+        from .index_space import IntVect as IV
+        d = self._dim
+        local, pairs = {}, {}
+        for row in self.rows():
+            lo = IV(*row[2:2 + d])
+            hi = IV(*row[5:5 + d])
+            s = tuple(int(v) for v in row[8:8 + d])
+            dst = Box(lo, hi, self._ixtype)
+            seg = CopySegment(int(row[0]), int(row[1]), dst.shift(tuple(-v for v in s)), dst, s)
+            sr, dr = int(row[11]), int(row[12])
+            if sr == dr:
+                local.setdefault(sr, []).append(seg)
+            else:
+                pairs.setdefault((sr, dr), []).append(seg)
+        self._groups = (local, pairs)
+
+    @property
+    def local_by_rank(self) -> dict:
+        if self._groups is None:
+            self._build_groups()
+        return self._groups[0]
+
+    @property
+    def pair_segments(self) -> dict:
+        if self._groups is None:
+            self._build_groups()
+        return self._groups[1]
+
+    def sends_from(self, rank: int) -> dict:
+        return {d: segs for (s, d), segs in sorted(self.pair_segments.items()) if s == rank}
+
+    def recvs_to(self, rank: int) -> dict:
+        return {s: segs for (s, d), segs in sorted(self.pair_segments.items()) if d == rank}
+
+    def executor(self, rank, kind, src_mf, dst_mf, scomp, dcomp, ncomp) -> "Executor":
+        key = (rank, kind, src_mf.ngrow.comps, src_mf.ncomp, dst_mf.ngrow.comps, dst_mf.ncomp,
+               scomp, dcomp, ncomp, dst_mf.dtype.itemsize, dst_mf.device)
+        with self._lock:
+            ex = self._execs.get(key)
+            if ex is None:
+                ex = Executor(self, rank, kind, src_mf.storage_rows(), src_mf.ncomp, dst_mf.storage_rows(),
+                              dst_mf.ncomp, scomp, dcomp, ncomp, dst_mf.dtype.itemsize, dst_mf.device)
+                self._execs[key] = ex
+        return ex
+
+    def __del__(self):
+        try:
+            self._execs.clear()
+            if self._h:
+                N.lib.ghx_plan_free(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
+class Executor:
+    """One rank's compiled share of a plan for one storage layout (a device
+    tag table; ``run`` is one launch of the fused copy kernel)."""
+
+    def __init__(self, plan, rank, kind, src_rows, src_nc, dst_rows, dst_nc, scomp, dcomp, ncomp, item, device):
+        h = C.c_void_p()
+        N.check(N.lib.ghx_exec_create(plan._h, rank, kind, N.i64p(src_rows), src_nc, N.i64p(dst_rows), dst_nc,
+                                      scomp, dcomp, ncomp, item, device, C.byref(h)))
+        self._h = h
+        self.plan = plan
+        self.nsrc = len(src_rows)
+        self.ndst = len(dst_rows)
+        self.nranks = plan.nranks
+        self.nptrs = self.nsrc + self.ndst + 2 * self.nranks
+        a, b, c, d = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+        N.check(N.lib.ghx_exec_info(h, C.byref(a), C.byref(b), C.byref(c), C.byref(d)))
+        self.ntags, self.ntasks, self.elems, self.alg_bytes = a.value, b.value, c.value, d.value
+        be = np.zeros(self.nranks, np.int64)
+        N.check(N.lib.ghx_exec_buffer_elems(h, N.i64p(be)))
+        self.buffer_elems = be
+
+    def run(self, table: np.ndarray, stream: int) -> None:
+        assert table.dtype == np.uint64 and table.size == self.nptrs
+        N.check(N.lib.ghx_exec_run(self._h, table.ctypes.data_as(C.POINTER(C.c_void_p)), self.nptrs,
+                                   C.c_void_p(stream)))
+
+    def set_grid(self, blocks: int) -> None:
+        N.check(N.lib.ghx_exec_set_grid(self._h, int(blocks), 256))
+
+    def __del__(self):
+        try:
+            if self._h:
+                N.lib.ghx_exec_free(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
+def _native_plan(gkey, build) -> int:
+    with _plan_lock:
+        plan = _global_plans.get(gkey)
+    if plan is not None:
+        return plan
+    plan = build()
+    with _plan_lock:
+        return _global_plans.setdefault(gkey, plan)
+
+
+def plan_build_fill_boundary(mf: MultiFab, geom: Geometry | None = None) -> CommPlan:
+    """Ghost-exchange plan for mf, cached on the MultiFab by PlanKey
+    (reference comm.py:289-309: same checks, same order)."""
+    geom = geom or mf.geom
+    if geom is None:
+        raise ValueError("fill_boundary needs a Geometry (periodicity)")
+    if mf.ba.ixtype.is_mixed:
+        raise ValueError("ghost exchange supports cell or fully-nodal index types only")
+    key = PlanKey(mf.ba.uid, mf.dm.uid, mf.ba.uid, mf.dm.uid, (0,) * len(mf.ngrow), mf.ngrow.comps,
+                  mf.ba.ixtype.flags, geom.periodic, "fill_boundary")
+    plan = mf.plan_cache.get(key)
+    if plan is not None:
+        return plan
+    if max(mf.ngrow) > mf.ba.minimal_extent():
+        raise ValueError("ngrow larger than the smallest box extent is not supported")
+    per = np.zeros(3, np.int32)
+    per[:len(geom.periodic)] = geom.periodic
+    period = np.ones(3, np.int64)
+    period[:len(geom.period)] = geom.period
+    ng = np.zeros(3, np.int64)
+    ng[:len(mf.ngrow)] = mf.ngrow.comps
+    ranks = mf.dm.array()
+
+    def build():
+        h = C.c_void_p()
+        N.check(N.lib.ghx_plan_build_fill_boundary(len(mf.ba), N.i64p(mf.ba.rows()), N.i64p(ng), N.i32p(per),
+                                                   N.i64p(period), N.i32p(ranks), mf.dm.nranks, C.byref(h)))
+        return CommPlan(h.value, mf.dm.nranks, len(mf.ngrow), mf.ba.ixtype)
+
+    plan = _native_plan((key, tuple(period)), build)
+    mf.plan_cache[key] = plan
+    mf.plan_builds += 1
+    return plan
+
+
+def _parallel_copy_plan(dst: MultiFab, src: MultiFab, gs: IntVect, gd: IntVect, geom) -> CommPlan:
+    key = PlanKey(src.ba.uid, src.dm.uid, dst.ba.uid, dst.dm.uid, gs.comps, gd.comps, dst.ba.ixtype.flags,
+                  geom.periodic if geom else (False,) * len(gs), "parallel_copy")
+    plan = dst.plan_cache.get(key)
+    if plan is not None:
+        return plan
+    nranks = max(src.dm.nranks, dst.dm.nranks)
+    gsa = np.zeros(3, np.int64)
+    gsa[:len(gs)] = gs.comps
+    gda = np.zeros(3, np.int64)
+    gda[:len(gd)] = gd.comps
+    per = period = None
+    if geom is not None:
+        per = np.zeros(3, np.int32)
+        per[:len(geom.periodic)] = geom.periodic
+        period = np.ones(3, np.int64)
+        period[:len(geom.period)] = geom.period
+
+    def build():
+        h = C.c_void_p()
+        N.check(N.lib.ghx_plan_build_parallel_copy(
+            len(dst.ba), N.i64p(dst.ba.rows()), N.i64p(gda), len(src.ba), N.i64p(src.ba.rows()), N.i64p(gsa),
+            N.i32p(per) if per is not None else None, N.i64p(period) if period is not None else None,
+            N.i32p(src.dm.array()), N.i32p(dst.dm.array()), nranks, C.byref(h)))
+        return CommPlan(h.value, nranks, len(gs), dst.ba.ixtype)
+
+    plan = _native_plan((key, None if period is None else tuple(period)), build)
+    dst.plan_cache[key] = plan
+    dst.plan_builds += 1
+    return plan
+
+
+# ------------------------------------------------------------------ execution
+
+TRANSPORTS = ("p2p", "nccl")
+
+
+def _transport() -> str:
+    t = os.environ.get("GHX_TRANSPORT", "p2p")
+    if t not in TRANSPORTS:
+        raise ValueError(f"GHX_TRANSPORT must be one of {TRANSPORTS}, got {t!r}")
+    return t
+
+
+def _stream(device: int):
+    import torch
+    return torch.cuda.current_stream(device)
+
+
+def _table(ex: Executor, src_mf: MultiFab, dst_parts, bufs=None) -> np.ndarray:
+    """Pointer table [src fabs][dst fabs][send bufs][recv bufs]."""
+    t = np.zeros(ex.nptrs, np.uint64)
+    if src_mf.local_indices:
+        t[np.asarray(src_mf.local_indices, np.int64)] = src_mf._ptrs
+    for idx, ptrs in dst_parts:
+        if len(idx):
+            t[ex.nsrc + np.asarray(idx, np.int64)] = ptrs
+    if bufs is not None:
+        t[ex.nsrc + ex.ndst:] = bufs
+    return t
+
+
+def _account(ctx, plan: CommPlan, me: int, ncomp: int, item: int) -> None:
+    row = plan.pair_cells[me]
+    for d in range(plan.nranks):
+        if d != me and row[d] > 0:
+            ctx.bus.account(me, d, int(row[d]) * ncomp * item)
+
+
+def _execute_plan(plan: CommPlan, src_mf: MultiFab, dst_mf: MultiFab, scomp: int, dcomp: int,
+                  ncomp: int, ctx, backend=None) -> None:
+    """Run ``plan`` for this rank (reference comm.py:316-380) on the current
+    torch stream of the MultiFab's device; returns when the data is in
+    place (the reference API is synchronous)."""
+    if src_mf.dtype != dst_mf.dtype:
+        raise ValueError("source and destination MultiFabs must share the real type")
+    me = ctx.rank
+    item = dst_mf.dtype.itemsize
+    dev = dst_mf.device
+    stream = _stream(dev)
+    if ctx.nranks == 1:
+        ex = plan.executor(me, N.EXEC_DIRECT, src_mf, dst_mf, scomp, dcomp, ncomp)
+        key = ("serial", src_mf.uid, dst_mf.uid, id(ex))
+        table = dst_mf._peer_cache.get(key)
+        if table is None:
+            table = _table(ex, src_mf, [(dst_mf.local_indices, dst_mf._ptrs)])
+            dst_mf._peer_cache[key] = table
+        ex.run(table, stream.cuda_stream)
+        stream.synchronize()
+        return
+    if ctx.kind == "thread":
+        _execute_threads(plan, src_mf, dst_mf, scomp, dcomp, ncomp, ctx, stream)
+    else:
+        _execute_process(plan, src_mf, dst_mf, scomp, dcomp, ncomp, ctx, stream)
+    _account(ctx, plan, me, ncomp, item)
+
+
+_peer_enabled: set = set()
+
+
+def _execute_threads(plan, src_mf, dst_mf, scomp, dcomp, ncomp, ctx, stream):
+    """Thread ranks: every rank's fabs are addressable from every rank (same
+    device, or peer access between devices), so remote tags are pushed by
+    the source rank's kernel directly into the receiver's ghost cells."""
+    me = ctx.rank
+    stream.synchronize()  # my earlier work on my fabs is done
+    infos = ctx.allgather((me, dst_mf.device, dst_mf.local_indices, dst_mf._ptrs))
+    for (_, d, _, _) in infos:
+        if d != dst_mf.device and (dst_mf.device, d) not in _peer_enabled:
+            N.check(N.lib.ghx_enable_peer_access(dst_mf.device, d))
+            _peer_enabled.add((dst_mf.device, d))
+    ex = plan.executor(me, N.EXEC_DIRECT, src_mf, dst_mf, scomp, dcomp, ncomp)
+    table = _table(ex, src_mf, [(idx, ptrs) for (_, _, idx, ptrs) in infos])
+    ex.run(table, stream.cuda_stream)
+    stream.synchronize()
+
+
+# -- process mode (one process per GPU) -------------------------------------
+
+class _ProcessSync:
+    """IPC-shared flag array per rank for the device-side barrier kernel."""
+
+    def __init__(self, ctx):
+        self.ctx = ctx
+        n = ctx.nranks
+        self.slab = Slab(8 * n, ctx.device)
+        N.check(N.lib.ghx_memset_u64(C.c_void_p(self.slab.ptr), 0, n, None))
+        import torch
+        torch.cuda.synchronize(ctx.device)
+        h = (C.c_uint8 * 64)()
+        N.check(N.lib.ghx_ipc_get_handle(C.c_void_p(self.slab.ptr), h))
+        handles = ctx.allgather(bytes(h))
+        self.ptrs = []
+        self._opened = []
+        for r, hb in enumerate(handles):
+            if r == ctx.rank:
+                self.ptrs.append(self.slab.ptr)
+                continue
+            p = C.c_void_p()
+            N.check(N.lib.ghx_ipc_open_handle(ctx.device, (C.c_uint8 * 64).from_buffer_copy(hb), C.byref(p)))
+            self.ptrs.append(p.value)
+            self._opened.append(p.value)
+        self.table = np.asarray(self.ptrs, np.uint64)
+        self.epoch = 0
+
+    def barrier(self, stream) -> None:
+        self.epoch += 1
+        N.check(N.lib.ghx_signal_barrier(self.table.ctypes.data_as(C.POINTER(C.c_void_p)), self.ctx.rank,
+                                         self.ctx.nranks, C.c_uint64(self.epoch), C.c_void_p(stream)))
+
+
+_psync: dict = {}
+
+
+def _process_sync(ctx) -> _ProcessSync:
+    key = (ctx.nranks, ctx.device)
+    s = _psync.get(key)
+    if s is None:
+        s = _psync[key] = _ProcessSync(ctx)
+    return s
+
+
+def _sync_mode(ctx) -> str:
+    m = os.environ.get("GHX_SYNC")
+    if m in ("host", "device"):
+        return m
+    # ranks sharing one GPU (tests) cannot spin-wait on each other
+    devs = ctx.allgather(ctx.device) if not hasattr(ctx, "_devs") else ctx._devs
+    ctx._devs = devs
+    return "device" if len(set(devs)) == len(devs) else "host"
+
+
+def _ipc_peers(ctx, mf: MultiFab):
+    """(indices, pointers) of every rank's fabs of ``mf``'s layout, mapped
+    into this process with CUDA IPC (cached on the MultiFab)."""
+    cache = mf._peer_cache.get("ipc")
+    if cache is not None:
+        return cache
+    h = (C.c_uint8 * 64)()
+    have = mf._slab is not None
+    if have:
+        N.check(N.lib.ghx_ipc_get_handle(C.c_void_p(mf._slab.ptr), h))
+    offs = [int(p) - mf._slab.ptr for p in mf._ptrs] if have else []
+    infos = ctx.allgather((ctx.rank, bytes(h) if have else None, mf.local_indices, offs))
+    parts, opened = [], []
+    for (r, hb, idx, off) in infos:
+        if r == ctx.rank:
+            parts.append((mf.local_indices, mf._ptrs))
+            continue
+        if hb is None:
+            continue
+        p = C.c_void_p()
+        N.check(N.lib.ghx_ipc_open_handle(mf.device, (C.c_uint8 * 64).from_buffer_copy(hb), C.byref(p)))
+        opened.append(p.value)
+        parts.append((idx, np.asarray([p.value + o for o in off], np.uint64)))
+    cache = (parts, opened)
+    mf._peer_cache["ipc"] = cache
+    weakref.finalize(mf, _close_ipc, list(opened))
+    return cache
+
+
+def _close_ipc(ptrs):
+    for p in ptrs:
+        try:
+            N.lib.ghx_ipc_close_handle(C.c_void_p(p))
+        except Exception:
+            pass
+
+
+def _execute_process(plan, src_mf, dst_mf, scomp, dcomp, ncomp, ctx, stream):
+    if _transport() == "nccl":
+        _execute_nccl(plan, src_mf, dst_mf, scomp, dcomp, ncomp, ctx, stream)
+        return
+    parts, _ = _ipc_peers(ctx, dst_mf)
+    ex = plan.executor(ctx.rank, N.EXEC_DIRECT, src_mf, dst_mf, scomp, dcomp, ncomp)
+    key = ("ipc", src_mf.uid, dst_mf.uid, id(ex))
+    table = dst_mf._peer_cache.get(key)
+    if table is None:
+        table = _table(ex, src_mf, parts)
+        dst_mf._peer_cache[key] = table
+    if _sync_mode(ctx) == "device":
+        sync = _process_sync(ctx)
+        sync.barrier(stream.cuda_stream)  # peers finished earlier work on their fabs
+        ex.run(table, stream.cuda_stream)
+        sync.barrier(stream.cuda_stream)  # every push into my fabs has landed
+        stream.synchronize()
+    else:
+        stream.synchronize()
+        ctx.barrier()
+        ex.run(table, stream.cuda_stream)
+        stream.synchronize()
+        ctx.barrier()
+
+
+def _execute_nccl(plan, src_mf, dst_mf, scomp, dcomp, ncomp, ctx, stream):
+    """Fallback: pack kernel -> one NCCL send/recv per ordered pair (grouped)
+    -> unpack kernel, plus the local kernel (comm.py:338-380 structure)."""
+    import torch.distributed as dist
+    me = ctx.rank
+    pack = plan.executor(me, N.EXEC_PACK, src_mf, dst_mf, scomp, dcomp, ncomp)
+    unpack = plan.executor(me, N.EXEC_UNPACK, src_mf, dst_mf, scomp, dcomp, ncomp)
+    local = plan.executor(me, N.EXEC_LOCAL, src_mf, dst_mf, scomp, dcomp, ncomp)
+    key = ("nccl", src_mf.uid, dst_mf.uid, id(pack))
+    cached = dst_mf._peer_cache.get(key)
+    if cached is None:
+        item = dst_mf.dtype.itemsize
+        n = plan.nranks
+        send_el, recv_el = pack.buffer_elems, unpack.buffer_elems
+        slab_s = Slab(max(1, int(send_el.sum()) * item + 256 * n), dst_mf.device)
+        slab_r = Slab(max(1, int(recv_el.sum()) * item + 256 * n), dst_mf.device)
+        ts, tr = slab_s.tensor(dst_mf.dtype), slab_r.tensor(dst_mf.dtype)
+        sbufs, rbufs = np.zeros(n, np.uint64), np.zeros(n, np.uint64)
+        send_t, recv_t = {}, {}
+        off_s = off_r = 0
+        for r in range(n):
+            if send_el[r]:
+                sbufs[r] = slab_s.ptr + off_s * item
+                send_t[r] = ts[off_s:off_s + int(send_el[r])]
+                off_s += -(-int(send_el[r]) * item // 256) * 256 // item
+            if recv_el[r]:
+                rbufs[r] = slab_r.ptr + off_r * item
+                recv_t[r] = tr[off_r:off_r + int(recv_el[r])]
+                off_r += -(-int(recv_el[r]) * item // 256) * 256 // item
+        bufs = np.concatenate([sbufs, rbufs])
+        own = [(dst_mf.local_indices, dst_mf._ptrs)]
+        cached = (_table(pack, src_mf, own, bufs), _table(unpack, src_mf, own, bufs),
+                  _table(local, src_mf, own, bufs), send_t, recv_t, (slab_s, slab_r))
+        dst_mf._peer_cache[key] = cached
+    t_pack, t_unpack, t_local, send_t, recv_t, _ = cached
+    pack.run(t_pack, stream.cuda_stream)
+    ops = [dist.P2POp(dist.isend, t, r) for r, t in sorted(send_t.items())]
+    ops += [dist.P2POp(dist.irecv, t, r) for r, t in sorted(recv_t.items())]
+    reqs = dist.batch_isend_irecv(ops) if ops else []
+    local.run(t_local, stream.cuda_stream)
+    for q in reqs:
+        q.wait()
+    unpack.run(t_unpack, stream.cuda_stream)
+    stream.synchronize()
+
+
+# --------------------------------------------------------------- public entry
+
+def fill_boundary(mf: MultiFab, geom: Geometry | None = None, backend=None) -> None:
+    """Fill every coverable ghost cell of ``mf`` from (periodically shifted)
+    valid data.  Collective over ranks; at most one message per ordered rank
+    pair; physical-boundary ghosts with no source and all valid cells are
+    left untouched (reference comm.py:383-394)."""
+    plan = plan_build_fill_boundary(mf, geom)
+    if plan.is_empty:
+        return
+    ctx = current_ctx()
+    _execute_plan(plan, mf, mf, 0, 0, mf.ncomp, ctx, backend)
+    ctx.barrier()
+
+
+def parallel_copy(dst: MultiFab, src: MultiFab, scomp: int = 0, dcomp: int = 0, ncomp: int | None = None,
+                  ngrow_src=0, ngrow_dst=0, geom: Geometry | None = None, backend=None) -> None:
+    """Copy src's (grown) valid data into every overlapping cell of dst's
+    (grown) boxes; periodic images only with ``geom`` (comm.py:397-429)."""
+    if src.ba.ixtype != dst.ba.ixtype:
+        raise ValueError("parallel_copy requires matching index types")
+    ncomp = ncomp if ncomp is not None else min(src.ncomp - scomp, dst.ncomp - dcomp)
+    if scomp < 0 or scomp + ncomp > src.ncomp or dcomp < 0 or dcomp + ncomp > dst.ncomp or ncomp < 1:
+        raise ValueError(f"component range out of bounds: scomp={scomp} dcomp={dcomp} ncomp={ncomp}")
+    gs = ngrow_src if isinstance(ngrow_src, IntVect) else IntVect.filled(ngrow_src)
+    gd = ngrow_dst if isinstance(ngrow_dst, IntVect) else IntVect.filled(ngrow_dst)
+    plan = _parallel_copy_plan(dst, src, gs, gd, geom)
+    if plan.is_empty:
+        return
+    ctx = current_ctx()
+    _execute_plan(plan, src, dst, scomp, dcomp, ncomp, ctx, backend)
+    ctx.barrier()

@@ -1,0 +1,487 @@
+"""Fab / BoxArray / DistributionMapping / MultiFab with fab storage in HBM.
+
+Drop-in for the reference's ``miniamr_core.mesh`` (core/mesh.py:38-325) on
+the exchange path.  Differences that follow from living on a B200:
+
+* storage is one device slab per MultiFab (``ghx_device_alloc``), carved
+  into 256-byte aligned fabs; each ``Fab.data`` is a zero-copy torch CUDA
+  tensor of shape (nx, ny, nz, ncomp) with F-order strides (1, nx, nx*ny,
+  nx*ny*nz) -- the same layout law as core/mesh.py:38-58 and
+  tests/test_mesh.py:67-80, offset (i-lo0) + ex0*((j-lo1) + ex1*((k-lo2) +
+  ex2*c));
+* ``memory="pinned"`` puts the slab in mapped, page-locked host memory: the
+  same exchange kernel then runs over PCIe on host-resident fabs (used for
+  the end-to-end host-buffer measurement);
+* ``BoxArray`` disjointness is checked by the native binned sweep instead
+  of the O(n^2) pair loop (core/mesh.py:203-205, 126 s at 4,096 boxes).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import itertools
+import math
+import threading
+from typing import Iterable, Iterator, Sequence
+
+import numpy as np
+
+from . import _native as N
+from . import config
+from .index_space import Box, Geometry, IndexType, IntVect, grow
+
+_uid_lock = threading.Lock()
+_uid_iter = itertools.count(1)
+
+
+def _next_uid() -> int:
+    with _uid_lock:
+        return next(_uid_iter)
+
+
+def _pad3(vals: Sequence[int], fill: int) -> tuple:
+    v = tuple(int(x) for x in vals)
+    return v + (fill,) * (3 - len(v))
+
+
+def storage_shape(box: Box, ncomp: int) -> tuple:
+    """(nx, ny, nz, ncomp), trailing spatial axes of extent 1 below 3-D."""
+    return _pad3(box.extents, 1) + (int(ncomp),)
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _torch_dtype(dt: np.dtype):
+    torch = _torch()
+    return torch.float64 if np.dtype(dt).itemsize == 8 else torch.float32
+
+
+def _current_device() -> int:
+    from . import comm
+    return comm.current_ctx().device
+
+
+class Slab:
+    """One native allocation (device HBM or pinned host), freed on GC."""
+
+    def __init__(self, nbytes: int, device: int, memory: str = "device"):
+        if memory not in ("device", "pinned"):
+            raise ValueError(f"memory must be 'device' or 'pinned', got {memory!r}")
+        p = C.c_void_p()
+        if memory == "device":
+            N.check(N.lib.ghx_device_alloc(int(device), -(-int(nbytes) // 256) * 256, C.byref(p)))
+        else:
+            N.check(N.lib.ghx_host_alloc(-(-int(nbytes) // 256) * 256, C.byref(p)))
+        self.ptr = int(p.value)
+        self.nbytes = int(nbytes)
+        self.device = int(device)
+        self.memory = memory
+
+    @property
+    def __cuda_array_interface__(self):
+        return {"shape": (self.nbytes,), "typestr": "|u1", "data": (self.ptr, False),
+                "version": 3, "strides": None}
+
+    @property
+    def __array_interface__(self):
+        if self.memory != "pinned":
+            raise AttributeError("device slab has no host array interface")
+        return {"shape": (self.nbytes,), "typestr": "|u1", "data": (self.ptr, False), "version": 3}
+
+    def tensor(self, dtype):
+        """1-D torch tensor over the whole slab (keeps the slab alive)."""
+        torch = _torch()
+        if self.memory == "device":
+            t = torch.as_tensor(self, device=f"cuda:{self.device}")
+        else:
+            t = torch.from_numpy(np.asarray(self))
+        return t.view(_torch_dtype(dtype))
+
+    def __del__(self):
+        try:
+            if self.ptr:
+                (N.lib.ghx_device_free if self.memory == "device" else N.lib.ghx_host_free)(C.c_void_p(self.ptr))
+                self.ptr = 0
+        except Exception:
+            pass
+
+
+class Fab:
+    """Multi-component real array over a Box, F-order, on the device."""
+
+    def __init__(self, box: Box, ncomp: int, arena=None, *, device: int | None = None,
+                 memory: str = "device", _slab=None, _offset: int = 0):
+        if box.is_empty:
+            raise ValueError("cannot create a Fab over an empty box")
+        if ncomp < 1:
+            raise ValueError(f"ncomp must be >= 1, got {ncomp}")
+        self.box = box
+        self.ncomp = int(ncomp)
+        self.dtype = config.real_dtype
+        shape = storage_shape(box, ncomp)
+        count = math.prod(shape)
+        if _slab is None:
+            dev = _current_device() if device is None else int(device)
+            _slab = Slab(count * self.dtype.itemsize, dev, memory)
+            _offset = 0
+            if config.debug:
+                N.check(N.lib.ghx_memset_u64(C.c_void_p(_slab.ptr), config.POISON_BITS64 if self.dtype.itemsize == 8
+                                             else (config.POISON_BITS32 << 32) | config.POISON_BITS32,
+                                             -(-count * self.dtype.itemsize // 8), None))
+        self._slab = _slab
+        self.device = _slab.device
+        self.memory = _slab.memory
+        flat = _slab.tensor(self.dtype)
+        nx, ny, nz, nc = shape
+        self.data = flat.as_strided(shape, (1, nx, nx * ny, nx * ny * nz), _offset)
+        self.ptr = _slab.ptr + _offset * self.dtype.itemsize
+        self.nbytes = count * self.dtype.itemsize
+
+    @property
+    def lo3(self) -> tuple:
+        return _pad3(self.box.lo, 0)
+
+    def raw(self):
+        """Flat storage in layout order (zero-copy)."""
+        return self.data.as_strided((self.data.numel(),), (1,))
+
+    def view(self, writable: bool = True) -> "FabView":
+        return FabView(self.data, self.lo3, self.ncomp, writable)
+
+    def setval(self, value: float, region: Box | None = None, comp_range=None) -> None:
+        fab_setval(self, value, region, comp_range)
+
+    def release(self) -> None:
+        self.data = None
+        self._slab = None
+
+
+def fab_create(box: Box, ncomp: int, arena=None) -> Fab:
+    return Fab(box, ncomp, arena)
+
+
+def _comp_slice(comp_range, ncomp: int) -> slice:
+    if comp_range is None:
+        return slice(0, ncomp)
+    if isinstance(comp_range, int):
+        if not 0 <= comp_range < ncomp:
+            raise ValueError(f"component {comp_range} out of range [0,{ncomp})")
+        return slice(comp_range, comp_range + 1)
+    a, b = comp_range
+    if not 0 <= a <= b <= ncomp:
+        raise ValueError(f"component range {comp_range} out of range [0,{ncomp}]")
+    return slice(a, b)
+
+
+def _region_slices(fab_box: Box, region: Box) -> tuple:
+    lo, rlo, rhi = _pad3(fab_box.lo, 0), _pad3(region.lo, 0), _pad3(region.hi, 0)
+    return tuple(slice(b - a, c - a + 1) for a, b, c in zip(lo, rlo, rhi))
+
+
+def fab_setval(f: Fab, value: float, region: Box | None = None, comp_range=None) -> None:
+    region = f.box if region is None else region
+    if region.is_empty:
+        return
+    if not f.box.contains(region):
+        raise ValueError(f"setval region {region} is not contained in fab box {f.box}")
+    sx, sy, sz = _region_slices(f.box, region)
+    f.data[sx, sy, sz, _comp_slice(comp_range, f.ncomp)] = value
+
+
+class FabView:
+    """Globally indexed accessor over a fab's (nx, ny, nz, ncomp) tensor.
+
+    Index with ints (returns a Python float) or integer arrays (returns a
+    tensor), as view[i, j, k], view[i, j, k, c] or in spacedim arity."""
+
+    __slots__ = ("_a", "lo3", "ncomp", "writable")
+
+    def __init__(self, data, lo3: tuple, ncomp: int, writable: bool):
+        self._a = data
+        self.lo3 = lo3
+        self.ncomp = ncomp
+        self.writable = writable
+
+    @property
+    def array(self):
+        return self._a
+
+    def _locate(self, idx):
+        torch = _torch()
+        if not isinstance(idx, tuple):
+            idx = (idx,)
+        n = len(idx)
+        if n == 4:
+            spatial, comp = idx[:3], idx[3]
+        elif n == 3:
+            spatial, comp = idx, 0
+        elif n == config.spacedim:
+            spatial, comp = tuple(idx) + (0,) * (3 - n), 0
+        else:
+            raise IndexError(f"expected (i,j,k[,c]) indices, got {n} entries")
+        out = []
+        scalar = isinstance(comp, (int, np.integer))
+        for d, v in enumerate(spatial):
+            if isinstance(v, (int, np.integer)):
+                li = int(v) - self.lo3[d]
+                if li < 0 or li >= self._a.shape[d]:
+                    raise IndexError(f"index {v} out of bounds on axis {d}")
+                out.append(li)
+            else:
+                scalar = False
+                t = torch.as_tensor(np.asarray(v) - self.lo3[d], device=self._a.device)
+                out.append(t)
+        out.append(comp)
+        return tuple(out), scalar
+
+    def __getitem__(self, idx):
+        loc, scalar = self._locate(idx)
+        v = self._a[loc]
+        return v.item() if scalar else v
+
+    def __setitem__(self, idx, value):
+        if not self.writable:
+            raise ValueError("assignment through a read-only FabView")
+        loc, _ = self._locate(idx)
+        torch = _torch()
+        if isinstance(value, np.ndarray):
+            value = torch.as_tensor(value, device=self._a.device, dtype=self._a.dtype)
+        self._a[loc] = value
+
+
+class BoxArray:
+    """Ordered, pairwise-disjoint valid boxes of one index type."""
+
+    def __init__(self, boxes: Iterable[Box], ixtype=None):
+        boxes = tuple(boxes)
+        self.uid = _next_uid()
+        if not boxes:
+            self.boxes = boxes
+            self.ixtype = ixtype if ixtype is not None else IndexType.cell()
+            self._rows = np.zeros((0, 6), np.int64)
+            self._dim = config.spacedim
+            return
+        t = boxes[0].ixtype
+        for b in boxes:
+            if b.is_empty:
+                raise ValueError("BoxArray boxes must be non-empty")
+            if b.ixtype != t:
+                raise ValueError("BoxArray boxes must share one index type")
+        rows = np.ascontiguousarray(np.array([b.as_row() for b in boxes], dtype=np.int64))
+        oa, ob = C.c_int64(), C.c_int64()
+        N.check(N.lib.ghx_boxes_disjoint(len(boxes), N.i64p(rows), C.byref(oa), C.byref(ob)))
+        if oa.value >= 0:
+            raise ValueError(f"BoxArray valid regions must be disjoint: {boxes[oa.value]} and "
+                             f"{boxes[ob.value]} overlap")
+        self.boxes = boxes
+        self.ixtype = t
+        self._rows = rows
+        self._dim = len(boxes[0].lo)
+        self._grown = {}
+
+    def __len__(self) -> int:
+        return len(self.boxes)
+
+    def __getitem__(self, i: int) -> Box:
+        return self.boxes[i]
+
+    def __iter__(self) -> Iterator[Box]:
+        return iter(self.boxes)
+
+    def minimal_extent(self) -> int:
+        r = self._rows
+        return int((r[:, 3:3 + self._dim] - r[:, :self._dim] + 1).min())
+
+    def rows(self, ngrow=None) -> np.ndarray:
+        """(n, 6) int64 lo/hi rows padded to 3 axes, optionally grown."""
+        if ngrow is None:
+            return self._rows
+        g = _pad3(ngrow, 0)
+        out = self._grown.get(g)
+        if out is None:
+            out = self._rows.copy()
+            out[:, :3] -= np.asarray(g, np.int64)
+            out[:, 3:] += np.asarray(g, np.int64)
+            out = np.ascontiguousarray(out)
+            self._grown[g] = out
+        return out
+
+
+def decompose(domain: Box, max_grid_size) -> BoxArray:
+    """Chop a domain into boxes of extent <= max_grid_size, x fastest."""
+    m = [max_grid_size] * len(domain.lo) if isinstance(max_grid_size, int) else list(max_grid_size)
+    per_axis = []
+    for lo, hi, s in zip(domain.lo, domain.hi, m):
+        starts = list(range(lo, hi + 1, s))
+        per_axis.append([(a, min(a + s - 1, hi)) for a in starts])
+    boxes = []
+    for combo in itertools.product(*per_axis[::-1]):
+        combo = combo[::-1]
+        boxes.append(Box([c[0] for c in combo], [c[1] for c in combo], domain.ixtype))
+    return BoxArray(boxes)
+
+
+class DistributionMapping:
+    """Owning rank per BoxArray entry."""
+
+    def __init__(self, rank_of: Iterable[int], nranks: int | None = None):
+        self.rank_of = tuple(int(r) for r in rank_of)
+        self.nranks = int(nranks) if nranks is not None else (max(self.rank_of) + 1 if self.rank_of else 1)
+        if any(r < 0 or r >= self.nranks for r in self.rank_of):
+            raise ValueError("rank ids must lie in [0, nranks)")
+        self.uid = _next_uid()
+        self._arr = np.ascontiguousarray(np.asarray(self.rank_of, dtype=np.int32))
+
+    @staticmethod
+    def round_robin(nboxes: int, nranks: int) -> "DistributionMapping":
+        return DistributionMapping([i % nranks for i in range(nboxes)], nranks)
+
+    def __len__(self) -> int:
+        return len(self.rank_of)
+
+    def __getitem__(self, i: int) -> int:
+        return self.rank_of[i]
+
+    def array(self) -> np.ndarray:
+        return self._arr
+
+
+_ALIGN = 256
+
+
+class MultiFab:
+    """BoxArray + DistributionMapping + ghost width + one device slab."""
+
+    def __init__(self, ba: BoxArray, dm: DistributionMapping, ncomp: int, ngrow,
+                 geom: Geometry | None = None, arena=None, rank: int | None = None,
+                 device: int | None = None, memory: str = "device"):
+        if len(ba) == 0:
+            raise ValueError("MultiFab needs a non-empty BoxArray")
+        if len(dm) != len(ba):
+            raise ValueError(f"distribution mapping length {len(dm)} != boxarray length {len(ba)}")
+        from . import comm
+        self.ba = ba
+        self.dm = dm
+        self.ncomp = int(ncomp)
+        if self.ncomp < 1:
+            raise ValueError(f"ncomp must be >= 1, got {ncomp}")
+        self.ngrow = ngrow if isinstance(ngrow, IntVect) else IntVect.filled(ngrow)
+        if any(g < 0 for g in self.ngrow):
+            raise ValueError("ngrow components must be >= 0")
+        self.geom = geom
+        self.dtype = config.real_dtype
+        ctx = comm.current_ctx()
+        self.rank = ctx.rank if rank is None else int(rank)
+        self.device = ctx.device if device is None else int(device)
+        self.memory = memory
+        self.local_indices = tuple(i for i, r in enumerate(dm.rank_of) if r == self.rank)
+        self.uid = _next_uid()
+        self.plan_cache: dict = {}
+        self.plan_builds = 0
+        self._peer_cache: dict = {}
+        self._alloc()
+
+    def _alloc(self) -> None:
+        item = self.dtype.itemsize
+        rows = self.ba.rows(self.ngrow)
+        offs = {}
+        total = 0
+        for i in self.local_indices:
+            r = rows[i]
+            count = int(np.prod(r[3:] - r[:3] + 1)) * self.ncomp
+            offs[i] = total // item
+            total += -(-count * item // _ALIGN) * _ALIGN
+        self._offsets = offs
+        self.fabs = {}
+        self._slab = None
+        if not self.local_indices:
+            self._ptrs = np.zeros(0, np.uint64)
+            return
+        self._slab = Slab(total, self.device, self.memory)
+        if config.debug:
+            N.check(N.lib.ghx_memset_u64(C.c_void_p(self._slab.ptr), config.POISON_BITS64 if item == 8
+                                         else (config.POISON_BITS32 << 32) | config.POISON_BITS32,
+                                         total // 8, None))
+        for i in self.local_indices:
+            self.fabs[i] = Fab(grow(self.ba[i], self.ngrow), self.ncomp, _slab=self._slab, _offset=offs[i])
+        self._ptrs = np.array([self.fabs[i].ptr for i in self.local_indices], np.uint64)
+
+    # -- reference surface (core/mesh.py:285-320)
+    def valid_box(self, i: int) -> Box:
+        return self.ba[i]
+
+    def grown_box(self, i: int) -> Box:
+        return grow(self.ba[i], self.ngrow)
+
+    def fab(self, i: int) -> Fab:
+        if i not in self.fabs:
+            raise KeyError(f"fab {i} is not owned by rank {self.rank}")
+        return self.fabs[i]
+
+    def view(self, i: int) -> FabView:
+        return self.fab(i).view(writable=True)
+
+    def const_view(self, i: int) -> FabView:
+        return self.fab(i).view(writable=False)
+
+    def arrays(self) -> list:
+        return [self.view(i) for i in self.local_indices]
+
+    def const_arrays(self) -> list:
+        return [self.const_view(i) for i in self.local_indices]
+
+    def local_boxes(self, grown: bool = False) -> list:
+        return [self.grown_box(i) if grown else self.ba[i] for i in self.local_indices]
+
+    def setval(self, value: float, comp_range=None, grown: bool = True) -> None:
+        for i in self.local_indices:
+            self.fabs[i].setval(value, self.grown_box(i) if grown else self.ba[i], comp_range)
+
+    def close(self) -> None:
+        for f in self.fabs.values():
+            f.release()
+        self.fabs = {}
+        self._slab = None
+        self._ptrs = np.zeros(0, np.uint64)
+
+    # -- exchange entry points named by the north star
+    def fill_boundary(self, geom: Geometry | None = None, backend=None) -> None:
+        from . import comm
+        comm.fill_boundary(self, geom, backend)
+
+    def parallel_copy(self, src: "MultiFab", scomp: int = 0, dcomp: int = 0, ncomp=None,
+                      ngrow_src=0, ngrow_dst=0, geom: Geometry | None = None, backend=None) -> None:
+        from . import comm
+        comm.parallel_copy(self, src, scomp, dcomp, ncomp, ngrow_src, ngrow_dst, geom, backend)
+
+    # -- synthetic data (bench / parity tests)
+    def fill_hash(self, seed: int, domain: Box, stream=None) -> None:
+        """Valid cells <- splitmix64 counter hash over ``domain`` (see
+        oracle/inputs.py for the formula), other cells <- sNaN poison."""
+        dom = np.ascontiguousarray(np.asarray(domain.as_row(), np.int64))
+        st = None if stream is None else C.c_void_p(stream)
+        for i in self.local_indices:
+            f = self.fabs[i]
+            fb = np.ascontiguousarray(np.asarray(f.box.as_row(), np.int64))
+            vb = np.ascontiguousarray(np.asarray(self.ba[i].as_row(), np.int64))
+            N.check(N.lib.ghx_fill_hash(C.c_void_p(f.ptr), N.i64p(fb), self.ncomp, N.i64p(vb), N.i64p(dom),
+                                        C.c_uint64(int(seed)), self.dtype.itemsize, st))
+
+    def storage_rows(self) -> np.ndarray:
+        return self.ba.rows(self.ngrow)
+
+
+def multifab_define(ba: BoxArray, dm: DistributionMapping, ncomp: int, ngrow,
+                    geom: Geometry | None = None, arena=None, **kw) -> MultiFab:
+    return MultiFab(ba, dm, ncomp, ngrow, geom, arena, **kw)
+
+
+def fab_view(mf: MultiFab, fab_index: int) -> FabView:
+    return mf.view(fab_index)
+
+
+def const_fab_view(mf: MultiFab, fab_index: int) -> FabView:
+    return mf.const_view(fab_index)

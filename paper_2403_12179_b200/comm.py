@@ -577,62 +577,8 @@ def _table(ex: Executor, src_mf: MultiFab, dst_parts, bufs=None) -> np.ndarray:
     return t
 
 
-def _account(ctx, plan: CommPlan, me: int, ncomp: int, item: int) -> None:
-    row = plan.pair_cells[me]
-    for d in range(plan.nranks):
-        if d != me and row[d] > 0:
-            ctx.bus.account(me, d, int(row[d]) * ncomp * item)
-
-
-def _execute_plan(plan: CommPlan, src_mf: MultiFab, dst_mf: MultiFab, scomp: int, dcomp: int,
-                  ncomp: int, ctx, backend=None) -> None:
-    """Run ``plan`` for this rank (reference comm.py:316-380) on the current
-    torch stream of the MultiFab's device; returns when the data is in
-    place (the reference API is synchronous)."""
-    if src_mf.dtype != dst_mf.dtype:
-        raise ValueError("source and destination MultiFabs must share the real type")
-    me = ctx.rank
-    item = dst_mf.dtype.itemsize
-    dev = dst_mf.device
-    stream = _stream(dev)
-    if ctx.nranks == 1:
-        ex = plan.executor(me, N.EXEC_DIRECT, src_mf, dst_mf, scomp, dcomp, ncomp)
-        key = ("serial", src_mf.uid, dst_mf.uid, id(ex))
-        table = dst_mf._peer_cache.get(key)
-        if table is None:
-            table = _table(ex, src_mf, [(dst_mf.local_indices, dst_mf._ptrs)])
-            dst_mf._peer_cache[key] = table
-        ex.run(table, stream.cuda_stream)
-        stream.synchronize()
-        return
-    if ctx.kind == "thread":
-        _execute_threads(plan, src_mf, dst_mf, scomp, dcomp, ncomp, ctx, stream)
-    else:
-        _execute_process(plan, src_mf, dst_mf, scomp, dcomp, ncomp, ctx, stream)
-    _account(ctx, plan, me, ncomp, item)
-
-
 _peer_enabled: set = set()
 
-
-def _execute_threads(plan, src_mf, dst_mf, scomp, dcomp, ncomp, ctx, stream):
-    """Thread ranks: every rank's fabs are addressable from every rank (same
-    device, or peer access between devices), so remote tags are pushed by
-    the source rank's kernel directly into the receiver's ghost cells."""
-    me = ctx.rank
-    stream.synchronize()  # my earlier work on my fabs is done
-    infos = ctx.allgather((me, dst_mf.device, dst_mf.local_indices, dst_mf._ptrs))
-    for (_, d, _, _) in infos:
-        if d != dst_mf.device and (dst_mf.device, d) not in _peer_enabled:
-            N.check(N.lib.ghx_enable_peer_access(dst_mf.device, d))
-            _peer_enabled.add((dst_mf.device, d))
-    ex = plan.executor(me, N.EXEC_DIRECT, src_mf, dst_mf, scomp, dcomp, ncomp)
-    table = _table(ex, src_mf, [(idx, ptrs) for (_, _, idx, ptrs) in infos])
-    ex.run(table, stream.cuda_stream)
-    stream.synchronize()
-
-
-# -- process mode (one process per GPU) -------------------------------------
 
 class _ProcessSync:
     """IPC-shared flag array per rank for the device-side barrier kernel."""
@@ -660,7 +606,7 @@ class _ProcessSync:
         self.table = np.asarray(self.ptrs, np.uint64)
         self.epoch = 0
 
-    def barrier(self, stream) -> None:
+    def barrier(self, stream: int) -> None:
         self.epoch += 1
         N.check(N.lib.ghx_signal_barrier(self.table.ctypes.data_as(C.POINTER(C.c_void_p)), self.ctx.rank,
                                          self.ctx.nranks, C.c_uint64(self.epoch), C.c_void_p(stream)))
@@ -678,12 +624,15 @@ def _process_sync(ctx) -> _ProcessSync:
 
 
 def _sync_mode(ctx) -> str:
+    """'device' (flag barrier kernels, no host round trip) when every rank
+    owns its own GPU; 'host' when ranks share a device (they cannot spin-wait
+    on each other) or GHX_SYNC=host."""
     m = os.environ.get("GHX_SYNC")
     if m in ("host", "device"):
         return m
-    # ranks sharing one GPU (tests) cannot spin-wait on each other
-    devs = ctx.allgather(ctx.device) if not hasattr(ctx, "_devs") else ctx._devs
-    ctx._devs = devs
+    devs = getattr(ctx, "_devs", None)
+    if devs is None:
+        devs = ctx._devs = ctx.allgather((os.uname().nodename, ctx.device))
     return "device" if len(set(devs)) == len(devs) else "host"
 
 
@@ -710,10 +659,9 @@ def _ipc_peers(ctx, mf: MultiFab):
         N.check(N.lib.ghx_ipc_open_handle(mf.device, (C.c_uint8 * 64).from_buffer_copy(hb), C.byref(p)))
         opened.append(p.value)
         parts.append((idx, np.asarray([p.value + o for o in off], np.uint64)))
-    cache = (parts, opened)
-    mf._peer_cache["ipc"] = cache
+    mf._peer_cache["ipc"] = parts
     weakref.finalize(mf, _close_ipc, list(opened))
-    return cache
+    return parts
 
 
 def _close_ipc(ptrs):
@@ -724,75 +672,168 @@ def _close_ipc(ptrs):
             pass
 
 
-def _execute_process(plan, src_mf, dst_mf, scomp, dcomp, ncomp, ctx, stream):
-    if _transport() == "nccl":
-        _execute_nccl(plan, src_mf, dst_mf, scomp, dcomp, ncomp, ctx, stream)
-        return
-    parts, _ = _ipc_peers(ctx, dst_mf)
-    ex = plan.executor(ctx.rank, N.EXEC_DIRECT, src_mf, dst_mf, scomp, dcomp, ncomp)
-    key = ("ipc", src_mf.uid, dst_mf.uid, id(ex))
-    table = dst_mf._peer_cache.get(key)
-    if table is None:
-        table = _table(ex, src_mf, parts)
-        dst_mf._peer_cache[key] = table
-    if _sync_mode(ctx) == "device":
-        sync = _process_sync(ctx)
-        sync.barrier(stream.cuda_stream)  # peers finished earlier work on their fabs
-        ex.run(table, stream.cuda_stream)
-        sync.barrier(stream.cuda_stream)  # every push into my fabs has landed
-        stream.synchronize()
-    else:
-        stream.synchronize()
-        ctx.barrier()
-        ex.run(table, stream.cuda_stream)
-        stream.synchronize()
-        ctx.barrier()
+class Exchange:
+    """A prepared FillBoundary / ParallelCopy for this rank: the compiled
+    executor(s), the pointer table and the synchronisation it needs.
 
+    ``enqueue(stream)`` puts the whole exchange on a CUDA stream without a
+    host round trip (serial; process mode with device barriers; NCCL
+    fallback) -- the FillBoundary_nowait analogue.  ``run()`` is the
+    synchronous reference contract (data in place, messages accounted)."""
 
-def _execute_nccl(plan, src_mf, dst_mf, scomp, dcomp, ncomp, ctx, stream):
-    """Fallback: pack kernel -> one NCCL send/recv per ordered pair (grouped)
-    -> unpack kernel, plus the local kernel (comm.py:338-380 structure)."""
-    import torch.distributed as dist
-    me = ctx.rank
-    pack = plan.executor(me, N.EXEC_PACK, src_mf, dst_mf, scomp, dcomp, ncomp)
-    unpack = plan.executor(me, N.EXEC_UNPACK, src_mf, dst_mf, scomp, dcomp, ncomp)
-    local = plan.executor(me, N.EXEC_LOCAL, src_mf, dst_mf, scomp, dcomp, ncomp)
-    key = ("nccl", src_mf.uid, dst_mf.uid, id(pack))
-    cached = dst_mf._peer_cache.get(key)
-    if cached is None:
-        item = dst_mf.dtype.itemsize
-        n = plan.nranks
-        send_el, recv_el = pack.buffer_elems, unpack.buffer_elems
-        slab_s = Slab(max(1, int(send_el.sum()) * item + 256 * n), dst_mf.device)
-        slab_r = Slab(max(1, int(recv_el.sum()) * item + 256 * n), dst_mf.device)
-        ts, tr = slab_s.tensor(dst_mf.dtype), slab_r.tensor(dst_mf.dtype)
+    def __init__(self, plan: CommPlan, src_mf: MultiFab, dst_mf: MultiFab, scomp: int, dcomp: int,
+                 ncomp: int, ctx):
+        if src_mf.dtype != dst_mf.dtype:
+            raise ValueError("source and destination MultiFabs must share the real type")
+        self.plan, self.src, self.dst, self.ctx = plan, src_mf, dst_mf, ctx
+        self.scomp, self.dcomp, self.ncomp = scomp, dcomp, ncomp
+        self.item = dst_mf.dtype.itemsize
+        self.device = dst_mf.device
+        me = ctx.rank
+        self.mode = "serial" if ctx.nranks == 1 else ctx.kind
+        self.transport = "p2p"
+        if self.mode == "process":
+            self.transport = _transport()
+            self.sync = _sync_mode(ctx) if self.transport == "p2p" else "stream"
+        else:
+            self.sync = "host" if self.mode == "thread" else "none"
+        if self.transport == "nccl":
+            self._init_nccl()
+        else:
+            self.ex = plan.executor(me, N.EXEC_DIRECT, src_mf, dst_mf, scomp, dcomp, ncomp)
+            if self.mode == "serial":
+                self.table = _table(self.ex, src_mf, [(dst_mf.local_indices, dst_mf._ptrs)])
+            elif self.mode == "process":
+                self.table = _table(self.ex, src_mf, _ipc_peers(ctx, dst_mf))
+                if self.sync == "device":
+                    self.psync = _process_sync(ctx)
+            else:
+                self.table = None  # thread ranks: gathered per call
+        row = plan.pair_cells[me]
+        self.messages = [(me, d, int(row[d]) * ncomp * self.item) for d in range(plan.nranks)
+                         if d != me and row[d] > 0]
+        # bytes moved by this rank's launch (local + pushed), read + write
+        self.local_cells = int(row[me])
+        self.remote_cells = int(sum(row[d] for d in range(plan.nranks) if d != me))
+        self.ghost_bytes = int(plan.pair_cells.sum()) * ncomp * self.item  # whole job, counted once
+
+    # -- NCCL fallback ---------------------------------------------------
+    def _init_nccl(self):
+        plan, src_mf, dst_mf, me = self.plan, self.src, self.dst, self.ctx.rank
+        a = (self.scomp, self.dcomp, self.ncomp)
+        self.pack = plan.executor(me, N.EXEC_PACK, src_mf, dst_mf, *a)
+        self.unpack = plan.executor(me, N.EXEC_UNPACK, src_mf, dst_mf, *a)
+        self.local = plan.executor(me, N.EXEC_LOCAL, src_mf, dst_mf, *a)
+        item, n = self.item, plan.nranks
+        send_el, recv_el = self.pack.buffer_elems, self.unpack.buffer_elems
+        self._slabs = (Slab(max(256, int(send_el.sum()) * item + 256 * n), dst_mf.device),
+                       Slab(max(256, int(recv_el.sum()) * item + 256 * n), dst_mf.device))
+        ts, tr = (sl.tensor(dst_mf.dtype) for sl in self._slabs)
         sbufs, rbufs = np.zeros(n, np.uint64), np.zeros(n, np.uint64)
-        send_t, recv_t = {}, {}
+        self.send_t, self.recv_t = {}, {}
         off_s = off_r = 0
         for r in range(n):
             if send_el[r]:
-                sbufs[r] = slab_s.ptr + off_s * item
-                send_t[r] = ts[off_s:off_s + int(send_el[r])]
+                sbufs[r] = self._slabs[0].ptr + off_s * item
+                self.send_t[r] = ts[off_s:off_s + int(send_el[r])]
                 off_s += -(-int(send_el[r]) * item // 256) * 256 // item
             if recv_el[r]:
-                rbufs[r] = slab_r.ptr + off_r * item
-                recv_t[r] = tr[off_r:off_r + int(recv_el[r])]
+                rbufs[r] = self._slabs[1].ptr + off_r * item
+                self.recv_t[r] = tr[off_r:off_r + int(recv_el[r])]
                 off_r += -(-int(recv_el[r]) * item // 256) * 256 // item
         bufs = np.concatenate([sbufs, rbufs])
         own = [(dst_mf.local_indices, dst_mf._ptrs)]
-        cached = (_table(pack, src_mf, own, bufs), _table(unpack, src_mf, own, bufs),
-                  _table(local, src_mf, own, bufs), send_t, recv_t, (slab_s, slab_r))
-        dst_mf._peer_cache[key] = cached
-    t_pack, t_unpack, t_local, send_t, recv_t, _ = cached
-    pack.run(t_pack, stream.cuda_stream)
-    ops = [dist.P2POp(dist.isend, t, r) for r, t in sorted(send_t.items())]
-    ops += [dist.P2POp(dist.irecv, t, r) for r, t in sorted(recv_t.items())]
-    reqs = dist.batch_isend_irecv(ops) if ops else []
-    local.run(t_local, stream.cuda_stream)
-    for q in reqs:
-        q.wait()
-    unpack.run(t_unpack, stream.cuda_stream)
-    stream.synchronize()
+        self.t_pack = _table(self.pack, src_mf, own, bufs)
+        self.t_unpack = _table(self.unpack, src_mf, own, bufs)
+        self.t_local = _table(self.local, src_mf, own, bufs)
+
+    def _enqueue_nccl(self, stream: int) -> None:
+        import torch.distributed as dist
+        self.pack.run(self.t_pack, stream)
+        ops = [dist.P2POp(dist.isend, t, r) for r, t in sorted(self.send_t.items())]
+        ops += [dist.P2POp(dist.irecv, t, r) for r, t in sorted(self.recv_t.items())]
+        reqs = dist.batch_isend_irecv(ops) if ops else []
+        self.local.run(self.t_local, stream)
+        for q in reqs:
+            q.wait()  # NCCL: the current stream waits, the host does not
+        self.unpack.run(self.t_unpack, stream)
+
+    # -- launching ---------------------------------------------------------
+    @property
+    def launches_per_call(self) -> int:
+        return 3 if self.transport == "nccl" else 1
+
+    def enqueue(self, stream: int) -> None:
+        if self.transport == "nccl":
+            self._enqueue_nccl(stream)
+        elif self.mode == "serial":
+            self.ex.run(self.table, stream)
+        elif self.mode == "process" and self.sync == "device":
+            self.psync.barrier(stream)  # peers finished earlier work on their fabs
+            self.ex.run(self.table, stream)
+            self.psync.barrier(stream)  # every push into my fabs has landed
+        else:
+            raise RuntimeError(f"{self.mode} ranks with host synchronisation cannot enqueue; use run()")
+
+    def run(self) -> None:
+        stream = _stream(self.device)
+        ctx = self.ctx
+        if self.mode == "thread":
+            stream.synchronize()  # my earlier work on my fabs is done
+            infos = ctx.allgather((ctx.rank, self.dst.device, self.dst.local_indices, self.dst._ptrs))
+            for (_, d, _, _) in infos:
+                if d != self.device and (self.device, d) not in _peer_enabled:
+                    N.check(N.lib.ghx_enable_peer_access(self.device, d))
+                    _peer_enabled.add((self.device, d))
+            table = _table(self.ex, self.src, [(idx, ptrs) for (_, _, idx, ptrs) in infos])
+            self.ex.run(table, stream.cuda_stream)
+            stream.synchronize()
+        elif self.mode == "process" and self.sync == "host":
+            stream.synchronize()
+            ctx.barrier()
+            self.ex.run(self.table, stream.cuda_stream)
+            stream.synchronize()
+            ctx.barrier()
+        else:
+            self.enqueue(stream.cuda_stream)
+            stream.synchronize()
+        for (s, d, nbytes) in self.messages:
+            ctx.bus.account(s, d, nbytes)
+
+
+def exchange_for(plan: CommPlan, src_mf: MultiFab, dst_mf: MultiFab, scomp: int, dcomp: int, ncomp: int,
+                 ctx=None) -> Exchange:
+    ctx = ctx or current_ctx()
+    key = ("xchg", plan.uid, src_mf.uid, scomp, dcomp, ncomp, ctx.kind, ctx.nranks,
+           _transport() if ctx.kind == "process" else None)
+    ex = dst_mf._peer_cache.get(key)
+    if ex is None:
+        ex = dst_mf._peer_cache[key] = Exchange(plan, src_mf, dst_mf, scomp, dcomp, ncomp, ctx)
+    return ex
+
+
+def _execute_plan(plan: CommPlan, src_mf: MultiFab, dst_mf: MultiFab, scomp: int, dcomp: int,
+                  ncomp: int, ctx, backend=None) -> None:
+    """Run ``plan`` for this rank (reference comm.py:316-380) on the current
+    torch stream of the MultiFab's device; returns when the data is in
+    place (the reference API is synchronous).  ``backend`` is accepted for
+    signature compatibility only: there is one execution path, the fused
+    CUDA kernel."""
+    exchange_for(plan, src_mf, dst_mf, scomp, dcomp, ncomp, ctx).run()
+
+
+def prepare_fill_boundary(mf: MultiFab, geom: Geometry | None = None) -> Exchange:
+    """Plan + compile the FillBoundary of ``mf`` once; the returned
+    Exchange can be enqueued on a stream repeatedly (FillBoundary_nowait)."""
+    plan = plan_build_fill_boundary(mf, geom)
+    return exchange_for(plan, mf, mf, 0, 0, mf.ncomp)
+
+
+def prepare_parallel_copy(dst: MultiFab, src: MultiFab, scomp: int = 0, dcomp: int = 0, ncomp=None,
+                          ngrow_src=0, ngrow_dst=0, geom: Geometry | None = None) -> Exchange:
+    ncomp, gs, gd = _pc_args(dst, src, scomp, dcomp, ncomp, ngrow_src, ngrow_dst)
+    plan = _parallel_copy_plan(dst, src, gs, gd, geom)
+    return exchange_for(plan, src, dst, scomp, dcomp, ncomp)
 
 
 # --------------------------------------------------------------- public entry
@@ -810,10 +851,7 @@ def fill_boundary(mf: MultiFab, geom: Geometry | None = None, backend=None) -> N
     ctx.barrier()
 
 
-def parallel_copy(dst: MultiFab, src: MultiFab, scomp: int = 0, dcomp: int = 0, ncomp: int | None = None,
-                  ngrow_src=0, ngrow_dst=0, geom: Geometry | None = None, backend=None) -> None:
-    """Copy src's (grown) valid data into every overlapping cell of dst's
-    (grown) boxes; periodic images only with ``geom`` (comm.py:397-429)."""
+def _pc_args(dst, src, scomp, dcomp, ncomp, ngrow_src, ngrow_dst):
     if src.ba.ixtype != dst.ba.ixtype:
         raise ValueError("parallel_copy requires matching index types")
     ncomp = ncomp if ncomp is not None else min(src.ncomp - scomp, dst.ncomp - dcomp)
@@ -821,6 +859,14 @@ def parallel_copy(dst: MultiFab, src: MultiFab, scomp: int = 0, dcomp: int = 0, 
         raise ValueError(f"component range out of bounds: scomp={scomp} dcomp={dcomp} ncomp={ncomp}")
     gs = ngrow_src if isinstance(ngrow_src, IntVect) else IntVect.filled(ngrow_src)
     gd = ngrow_dst if isinstance(ngrow_dst, IntVect) else IntVect.filled(ngrow_dst)
+    return ncomp, gs, gd
+
+
+def parallel_copy(dst: MultiFab, src: MultiFab, scomp: int = 0, dcomp: int = 0, ncomp: int | None = None,
+                  ngrow_src=0, ngrow_dst=0, geom: Geometry | None = None, backend=None) -> None:
+    """Copy src's (grown) valid data into every overlapping cell of dst's
+    (grown) boxes; periodic images only with ``geom`` (comm.py:397-429)."""
+    ncomp, gs, gd = _pc_args(dst, src, scomp, dcomp, ncomp, ngrow_src, ngrow_dst)
     plan = _parallel_copy_plan(dst, src, gs, gd, geom)
     if plan.is_empty:
         return

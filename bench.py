@@ -97,7 +97,9 @@ def layout(amr, cfg, G):
 
 def make_fields(amr, cfg, L, memory="device"):
     if cfg["kind"] == "fb":
-        mf = amr.MultiFab(L["ba"], L["dm"], cfg["ncomp"], cfg["ngrow"], L["geom"], memory=memory)
+        ng = cfg["ngrow"]
+        ng = amr.IntVect(*ng) if isinstance(ng, tuple) else ng
+        mf = amr.MultiFab(L["ba"], L["dm"], cfg["ncomp"], ng, L["geom"], memory=memory)
         mf.fill_hash(SEED, L["dom"])
         return mf, None
     src = amr.MultiFab(L["sba"], L["sdm"], cfg["ncomp"], 0, memory=memory)
@@ -388,7 +390,8 @@ def run_ours(args, cfg, rank, world):
                    "transport": x.transport if world > 1 else "local",
                    "l2": "flushed before every step (512 MiB write, outside the events)",
                    "tags_this_rank": x.ex.ntags if x.transport == "p2p" else None,
-                   "warp_tasks_this_rank": x.ex.ntasks if x.transport == "p2p" else None},
+                   "warp_tasks_this_rank": x.ex.ntasks if x.transport == "p2p" else None,
+                   "exec": x.ex.detail if x.transport == "p2p" else None},
         "roofline": roof, "gpu_launches": int(launches), "clocks": clk.result(),
         "plan_build_s": round(t_plan, 4), "exec_compile_s": round(t_exec, 4), "alloc_fill_s": round(t_alloc, 3),
         "verified": verified,
@@ -465,13 +468,18 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ngrow", default=None, help="diagnostic: override ghost width per axis, e.g. 2,0,0")
     args = ap.parse_args()
     if args.warmup < 3:
         log("[bench] warm-up raised to 3 (timing rules)")
         args.warmup = 3
     if args.transport:
         os.environ["GHX_TRANSPORT"] = args.transport
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.ngrow:
+        g = tuple(int(v) for v in args.ngrow.split(","))
+        cfg["ngrow"] = g if len(g) == 3 else g[0]
+        cfg["desc"] += f" [diagnostic ngrow={args.ngrow}]"
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if args.impl == "reference":

@@ -121,6 +121,9 @@ int ghx_exec_run(ghx_exec *ex, void *const *ptrs, int64_t nptrs, void *stream);
 int ghx_exec_info(const ghx_exec *ex, int64_t *ntags, int64_t *ntasks, int64_t *elems,
                   int64_t *alg_bytes);
 int ghx_exec_buffer_elems(const ghx_exec *ex, int64_t *per_peer);
+/* out[8] = tags, warp tasks, elements, algorithmic bytes, tags in mirror
+ * pairs, tags in sector-swap pairs, grid blocks, load flavour. */
+int ghx_exec_detail(const ghx_exec *ex, int64_t out[8]);
 
 /* Launch-time tuning knob (warps per block * blocks): 0 = default. */
 int ghx_exec_set_grid(ghx_exec *ex, int32_t blocks, int32_t threads);

@@ -452,6 +452,10 @@ class Executor:
         be = np.zeros(self.nranks, np.int64)
         N.check(N.lib.ghx_exec_buffer_elems(h, N.i64p(be)))
         self.buffer_elems = be
+        det = np.zeros(8, np.int64)
+        N.check(N.lib.ghx_exec_detail(h, N.i64p(det)))
+        self.detail = dict(zip(("tags", "tasks", "elems", "alg_bytes", "mirror_tags", "swap_tags", "blocks",
+                                "ld_mode"), (int(v) for v in det)))
 
     def run(self, table: np.ndarray, stream: int) -> None:
         assert table.dtype == np.uint64 and table.size == self.nptrs

@@ -14,21 +14,35 @@
 //   * GHX_EXEC_PACK / GHX_EXEC_UNPACK  the NCCL fallback's pack and unpack
 //                      (same per-peer F-order buffer layout as comm.py:341-377).
 //
-// Work decomposition: each tag is flattened to (x/vec, y, z, comp) with the
-// widest raw-word vector (16/8/4 B) its alignment allows (rows whose src
-// and dst share the same 16-byte phase are peeled into head/body/tail);
-// tags are cut into warp tasks of 32*U vectors; a persistent grid of warps
-// strides over the task list.  Each lane issues U independent vector loads
-// before its U stores.  Values are copied as raw words (never through FP
-// registers' arithmetic), so NaN payloads survive bit-exactly.
+// Work decomposition
+//   * each tag is flattened to (x/vec, y, z, comp) with the widest raw-word
+//     vector (16/8/4 B) its alignment allows (rows whose src and dst share
+//     the same 16-byte phase are peeled into head/body/tail);
+//   * a warp task is TWO chunks of 32*kU vectors: either a tag and its
+//     mirror (the tag that writes the other half of the same 32-byte
+//     sectors, e.g. fab A's x-lo ghosts <- fab L's last valid columns and
+//     L's x-hi ghosts <- A's first valid columns), so both halves of every
+//     touched sector are read and rewritten together and L2 merges the
+//     partial-sector writes instead of refilling them from HBM; or two
+//     consecutive chunks of one tag;
+//   * every lane issues its 2*kU vector loads before any store;
+//   * the grid is persistent; each warp owns a contiguous range of tasks,
+//     so the two tag descriptors it needs stay cached in shared memory;
+//   * descriptors carry absolute base addresses, bound once per pointer
+//     table by ghx_bind_kernel (no pointer-table load on the critical path).
+// Values are copied as raw words, so NaN payloads survive bit-exactly.
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
+#include <functional>
+#include <map>
 #include <mutex>
 #include <new>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "ghx_internal.h"
@@ -39,9 +53,11 @@ using ghx::set_error;
 
 namespace {
 
-constexpr int kU = 4;                 // vectors per lane per task
-constexpr int kTaskVecs = 32 * kU;    // vectors per warp task
+constexpr int kU = 4;               // vectors per lane per chunk
+constexpr int kChunk = 32 * kU;     // vectors per chunk (a task has two)
 constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kSwapSlots = 8;
 
 std::atomic<int64_t> g_launches{0};
 
@@ -61,132 +77,228 @@ FastDiv make_div(uint32_t d) {
 }
 
 struct __align__(16) DevTag {
-  int64_t src_off, dst_off;  // vectors
+  uint64_t src, dst;         // byte address of element (0,0,0,0); bound per pointer table
   int64_t src_sz, dst_sz;    // z stride, vectors
   int64_t src_sc, dst_sc;    // component stride, vectors
   int32_t src_sy, dst_sy;    // y stride, vectors
-  int32_t src_ptr, dst_ptr;  // pointer-table slots
   uint32_t nvec;             // nxv * ny * nz * nc
   uint32_t nxv, ny, nz;
   uint32_t mx, my, mz;       // fast-divmod multipliers
   uint8_t sx, sy, sz, vlog;  // shifts, log2(vector bytes)
+  int32_t src_ptr, dst_ptr;  // pointer-table slots (bind only)
+  int64_t src_off, dst_off;  // vectors from the slot's base (bind only)
 };
-static_assert(sizeof(DevTag) == 96, "DevTag layout");
+static_assert(sizeof(DevTag) == 112, "DevTag layout");
+constexpr int kTagVec = sizeof(DevTag) / 16;
 
 __device__ __forceinline__ uint32_t fdiv(uint32_t n, uint32_t d, uint32_t m, uint32_t s) {
   return d == 1 ? n : (__umulhi(n, m) >> s);
 }
 
-template <class V, bool NC>
-__device__ __forceinline__ V load_vec(const V *p);
+// Load flavours (template LD): 0 = ld.global.nc.L1::no_allocate (read-only
+// path), 1 = ld.global.L1::no_allocate, 2 = ld.global.cg (L2 only),
+// 3 = ld.global.cs (streaming), 4 = ld.global (default caching).
+#define GHX_LD(SUFFIX, TYPE, ...)                                                        \
+  if (LD == 0)                                                                           \
+    asm volatile("ld.global.nc.L1::no_allocate" SUFFIX : __VA_ARGS__);                  \
+  else if (LD == 1)                                                                      \
+    asm volatile("ld.global.L1::no_allocate" SUFFIX : __VA_ARGS__);                     \
+  else if (LD == 2)                                                                      \
+    asm volatile("ld.global.cg" SUFFIX : __VA_ARGS__);                                  \
+  else if (LD == 3)                                                                      \
+    asm volatile("ld.global.cs" SUFFIX : __VA_ARGS__);                                  \
+  else                                                                                   \
+    asm volatile("ld.global" SUFFIX : __VA_ARGS__);
 
-template <>
-__device__ __forceinline__ uint4 load_vec<uint4, true>(const uint4 *p) {
+template <int LD>
+__device__ __forceinline__ uint4 ld16(const void *p) {
   uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
+  GHX_LD(".v4.u32 {%0,%1,%2,%3}, [%4];", uint4, "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p))
   return r;
 }
-template <>
-__device__ __forceinline__ uint4 load_vec<uint4, false>(const uint4 *p) {
-  uint4 r;
-  asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-}
-template <>
-__device__ __forceinline__ uint2 load_vec<uint2, true>(const uint2 *p) {
+template <int LD>
+__device__ __forceinline__ uint2 ld8(const void *p) {
   uint2 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+  GHX_LD(".v2.u32 {%0,%1}, [%2];", uint2, "=r"(r.x), "=r"(r.y) : "l"(p))
   return r;
 }
-template <>
-__device__ __forceinline__ uint2 load_vec<uint2, false>(const uint2 *p) {
-  uint2 r;
-  asm volatile("ld.global.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
-  return r;
-}
-template <>
-__device__ __forceinline__ uint32_t load_vec<uint32_t, true>(const uint32_t *p) {
+template <int LD>
+__device__ __forceinline__ uint32_t ld4(const void *p) {
   uint32_t r;
-  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
-  return r;
-}
-template <>
-__device__ __forceinline__ uint32_t load_vec<uint32_t, false>(const uint32_t *p) {
-  uint32_t r;
-  asm volatile("ld.global.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+  GHX_LD(".u32 %0, [%1];", uint32_t, "=r"(r) : "l"(p))
   return r;
 }
 
-// (x, y, z, c) of flattened vector index v within tag t
-struct Coord {
-  uint32_t x, y, z, c;
+struct u8x32 {
+  uint32_t w[8];
 };
-__device__ __forceinline__ Coord coord_of(const DevTag *__restrict__ t, uint32_t v) {
-  const uint32_t nxv = t->nxv, ny = t->ny, nz = t->nz;
-  const uint32_t r = fdiv(v, nxv, t->mx, t->sx);
-  const uint32_t r2 = fdiv(r, ny, t->my, t->sy);
-  const uint32_t c = fdiv(r2, nz, t->mz, t->sz);
-  return Coord{v - r * nxv, r - r2 * ny, r2 - c * nz, c};
+template <int LD>
+__device__ __forceinline__ u8x32 ld32(const void *p) {
+  u8x32 r;
+  GHX_LD(".v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];", u8x32, "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]),
+         "=r"(r.w[3]), "=r"(r.w[4]), "=r"(r.w[5]), "=r"(r.w[6]), "=r"(r.w[7]) : "l"(p))
+  return r;
+}
+__device__ __forceinline__ void st32(void *p, const uint32_t (&w)[8]) {
+  asm volatile("st.global.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(w[0]), "r"(w[1]), "r"(w[2]),
+               "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+               : "memory");
 }
 
-template <class V, bool NC>
-__device__ __forceinline__ void copy_task(const DevTag *__restrict__ t, const char *sb, char *db,
-                                          uint32_t start, int lane) {
-  const V *__restrict__ s = reinterpret_cast<const V *>(sb) + t->src_off;
-  V *__restrict__ d = reinterpret_cast<V *>(db) + t->dst_off;
-  const uint32_t nvec = t->nvec;
-  V val[kU];
-  // all loads first (kU independent requests in flight per lane) ...
+// element offset (in vectors) of flattened vector index v, for src or dst
+template <bool SRC>
+__device__ __forceinline__ int64_t vec_offset(const DevTag &t, uint32_t v) {
+  const uint32_t r = fdiv(v, t.nxv, t.mx, t.sx);
+  const uint32_t r2 = fdiv(r, t.ny, t.my, t.sy);
+  const uint32_t c = fdiv(r2, t.nz, t.mz, t.sz);
+  const uint32_t x = v - r * t.nxv, y = r - r2 * t.ny, z = r2 - c * t.nz;
+  return SRC ? (int64_t)x + (int64_t)y * t.src_sy + (int64_t)z * t.src_sz + (int64_t)c * t.src_sc
+             : (int64_t)x + (int64_t)y * t.dst_sy + (int64_t)z * t.dst_sz + (int64_t)c * t.dst_sc;
+}
+
+template <int LD>
+__device__ __forceinline__ void load_chunk(const DevTag &t, uint32_t start, int lane, uint4 (&val)[kU]) {
+  const char *base = reinterpret_cast<const char *>(t.src);
+  const int vl = t.vlog;
 #pragma unroll
   for (int u = 0; u < kU; ++u) {
     const uint32_t v = start + (uint32_t)(u * 32 + lane);
-    if (v < nvec) {
-      const Coord q = coord_of(t, v);
-      val[u] = load_vec<V, NC>(s + ((int64_t)q.x + (int64_t)q.y * t->src_sy + (int64_t)q.z * t->src_sz +
-                                    (int64_t)q.c * t->src_sc));
+    if (v < t.nvec) {
+      const char *p = base + (vec_offset<true>(t, v) << vl);
+      if (vl == 4)
+        val[u] = ld16<LD>(p);
+      else if (vl == 3) {
+        const uint2 q = ld8<LD>(p);
+        val[u].x = q.x;
+        val[u].y = q.y;
+      } else
+        val[u].x = ld4<LD>(p);
     }
   }
-  // ... then the stores (destination offsets recomputed: ALU is cheaper
-  // than the registers needed to keep them)
+}
+
+__device__ __forceinline__ void store_chunk(const DevTag &t, uint32_t start, int lane, const uint4 (&val)[kU]) {
+  char *base = reinterpret_cast<char *>(t.dst);
+  const int vl = t.vlog;
 #pragma unroll
   for (int u = 0; u < kU; ++u) {
     const uint32_t v = start + (uint32_t)(u * 32 + lane);
-    if (v < nvec) {
-      const Coord q = coord_of(t, v);
-      d[(int64_t)q.x + (int64_t)q.y * t->dst_sy + (int64_t)q.z * t->dst_sz + (int64_t)q.c * t->dst_sc] = val[u];
+    if (v < t.nvec) {
+      char *p = base + (vec_offset<false>(t, v) << vl);
+      if (vl == 4)
+        *reinterpret_cast<uint4 *>(p) = val[u];
+      else if (vl == 3)
+        *reinterpret_cast<uint2 *>(p) = make_uint2(val[u].x, val[u].y);
+      else
+        *reinterpret_cast<uint32_t *>(p) = val[u].x;
     }
   }
+}
+
+// Sector swap for a mirror pair of 16-byte-row tags (T1 described by t,
+// T2 implied): T1 writes the low half of sector SA (fab A's first 32 bytes
+// of the row: ghost | first valid columns) from the low half of sector SL
+// (fab L's last 32 bytes: last valid columns | ghost); T2 writes the high
+// half of SL from the high half of SA.  Both sectors end up holding
+// (SL.lo, SA.hi): each lane reads two whole sectors and writes them back
+// whole, so L2 never refills a partially written sector from HBM.
+template <int LD>
+__device__ __noinline__ void swap_chunk(const DevTag &t, uint32_t start, int lane) {
+  constexpr int kS = kU / 2;
+  char *const da = reinterpret_cast<char *>(t.dst);
+  char *const sl = reinterpret_cast<char *>(t.src);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    u8x32 a[kS], l[kS];
+#pragma unroll
+    for (int u = 0; u < kS; ++u) {
+      const uint32_t v = start + (uint32_t)((h * kS + u) * 32 + lane);
+      if (v < t.nvec) {
+        a[u] = ld32<LD>(da + (vec_offset<false>(t, v) << 4));
+        l[u] = ld32<LD>(sl + (vec_offset<true>(t, v) << 4));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kS; ++u) {
+      const uint32_t v = start + (uint32_t)((h * kS + u) * 32 + lane);
+      if (v < t.nvec) {
+        const uint32_t w[8] = {l[u].w[0], l[u].w[1], l[u].w[2], l[u].w[3], a[u].w[4], a[u].w[5], a[u].w[6], a[u].w[7]};
+        st32(da + (vec_offset<false>(t, v) << 4), w);
+        st32(sl + (vec_offset<true>(t, v) << 4), w);
+      }
+    }
+  }
+}
+
+// cooperative 112-byte descriptor load into this warp's shared slot
+__device__ __forceinline__ void fetch_tag(const DevTag *__restrict__ tags, int idx, DevTag *slot, int lane) {
+  if (lane < kTagVec)
+    reinterpret_cast<uint4 *>(slot)[lane] = __ldg(reinterpret_cast<const uint4 *>(tags + idx) + lane);
 }
 
 }  // namespace
 
-template <bool NC>
+// Resolve pointer-table slots into absolute addresses (once per table).
+__global__ void ghx_bind_kernel(DevTag *tags, int ntags, void *const *__restrict__ ptrs) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ntags; i += gridDim.x * blockDim.x) {
+    DevTag &t = tags[i];
+    t.src = reinterpret_cast<uint64_t>(ptrs[t.src_ptr]) + ((uint64_t)t.src_off << t.vlog);
+    t.dst = reinterpret_cast<uint64_t>(ptrs[t.dst_ptr]) + ((uint64_t)t.dst_off << t.vlog);
+  }
+}
+
+// tasks: {tagA, startA, tagB (-1: none), startB}
+template <int LD>
 __global__ void __launch_bounds__(kThreads) ghx_copy_kernel(const DevTag *__restrict__ tags,
-                                                            const int2 *__restrict__ tasks, int ntasks,
-                                                            void *const *__restrict__ ptrs) {
+                                                            const int4 *__restrict__ tasks, int ntasks) {
+  __shared__ DevTag slots[kWarps][2];
+  __shared__ DevTag swc[kWarps][kSwapSlots];  // direct-mapped cache of sector-swap descriptors
+  __shared__ int swc_id[kWarps][kSwapSlots];
   const int lane = threadIdx.x & 31;
-  const int warp = (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
-  const int nwarps = (int)((gridDim.x * (unsigned)blockDim.x) >> 5);
-  for (int w = warp; w < ntasks; w += nwarps) {
-    const int2 tk = __ldg(tasks + w);
-    const DevTag *t = tags + tk.x;
-    const char *sb = static_cast<const char *>(ptrs[t->src_ptr]);
-    char *db = static_cast<char *>(ptrs[t->dst_ptr]);
-    switch (t->vlog) {
-      case 4:
-        copy_task<uint4, NC>(t, sb, db, (uint32_t)tk.y, lane);
-        break;
-      case 3:
-        copy_task<uint2, NC>(t, sb, db, (uint32_t)tk.y, lane);
-        break;
-      default:
-        copy_task<uint32_t, NC>(t, sb, db, (uint32_t)tk.y, lane);
-        break;
+  const int wib = threadIdx.x >> 5;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int first = (int)(warp * ntasks / nwarps);
+  const int last = (int)((warp + 1) * ntasks / nwarps);
+  DevTag &ta = slots[wib][0];
+  DevTag &tb = slots[wib][1];
+  int have_a = -1, have_b = -1;
+  if (lane < kSwapSlots) swc_id[wib][lane] = -1;
+  __syncwarp();
+  int4 tk = first < last ? __ldg(tasks + first) : make_int4(0, 0, -1, 0);
+  for (int w = first; w < last; ++w) {
+    const int4 nxt = (w + 1 < last) ? __ldg(tasks + w + 1) : tk;  // prefetch
+    if (tk.z == -2) {  // sector-swap task over one chunk of T1
+      const int sl = tk.x & (kSwapSlots - 1);
+      if (swc_id[wib][sl] != tk.x) {
+        __syncwarp();
+        fetch_tag(tags, tk.x, &swc[wib][sl], lane);
+        if (lane == 0) swc_id[wib][sl] = tk.x;
+        __syncwarp();
+      }
+      swap_chunk<LD>(swc[wib][sl], (uint32_t)tk.y, lane);
+      if (tk.w >= 0) swap_chunk<LD>(swc[wib][sl], (uint32_t)tk.w, lane);
+      tk = nxt;
+      continue;
     }
+    if (tk.x != have_a || tk.z != have_b) {
+      __syncwarp();
+      if (tk.x == have_b && tk.z == have_a) {  // swapped pair order: swap roles
+        tk = make_int4(tk.z, tk.w, tk.x, tk.y);
+      } else {
+        if (tk.x != have_a) fetch_tag(tags, tk.x, &ta, lane);
+        if (tk.z >= 0 && tk.z != have_b) fetch_tag(tags, tk.z, &tb, lane);
+        have_a = tk.x;
+        have_b = tk.z;
+      }
+      __syncwarp();
+    }
+    uint4 va[kU], vb[kU];
+    load_chunk<LD>(ta, (uint32_t)tk.y, lane, va);
+    if (tk.z >= 0) load_chunk<LD>(tb, (uint32_t)tk.w, lane, vb);
+    store_chunk(ta, (uint32_t)tk.y, lane, va);
+    if (tk.z >= 0) store_chunk(tb, (uint32_t)tk.w, lane, vb);
+    tk = nxt;
   }
 }
 
@@ -234,6 +346,8 @@ struct HostTag {
   Side s, d;
   int64_t nx, ny, nz, nc;  // elements
   bool remote;
+  int32_t sfab, dfab;      // plan fab ids (pairing)
+  int64_t shift[3];
 };
 
 int vec_log(const HostTag &t, int64_t eb, int64_t x0, int64_t nxe) {
@@ -246,8 +360,11 @@ int vec_log(const HostTag &t, int64_t eb, int64_t x0, int64_t nxe) {
     if ((t.d.sy * eb) % vb || (t.d.sz * eb) % vb || (t.d.sc * eb) % vb) continue;
     return vl;
   }
-  return -1;
+  return eb == 8 ? 3 : 2;
 }
+
+// pairing key of a device tag: (src fab, dst fab, shift, part, shape)
+using PairKey = std::tuple<int32_t, int32_t, int64_t, int64_t, int64_t, int, uint32_t, uint32_t, uint32_t, int>;
 
 }  // namespace
 
@@ -257,23 +374,28 @@ struct ghx_exec {
   int32_t nranks = 1, nsrc = 0, ndst = 0;
   int32_t elem_bytes = 8;
   bool nc_loads = true;
+  int ld_mode = 2;  // ld.global.cg measured best on B200 (see profiles/)
   int64_t elems = 0;
+  int64_t npaired = 0, nswap = 0;
+  std::vector<uint8_t> swap_fab;  // fabs touched by sector-swap tasks
   std::vector<int64_t> buf_elems;  // per peer (pack: send, unpack: recv)
   std::vector<DevTag> htags;
-  std::vector<int2> htasks;
+  std::vector<PairKey> hkeys;
+  std::vector<int32_t> hremote;
+  std::vector<int4> htasks;
   DevTag *dtags = nullptr;
-  int2 *dtasks = nullptr;
+  int4 *dtasks = nullptr;
   void **dptrs = nullptr;
   std::vector<void *> cached_ptrs;
   int64_t nptrs = 0;
   int blocks = 0, threads = kThreads;
+  bool uploaded = false;
   std::mutex mu;
 };
 
 namespace {
 
-void add_devtag(ghx_exec *ex, const HostTag &t, int64_t x0, int64_t nxe, int vl,
-                std::vector<int32_t> &tag_remote) {
+void add_devtag(ghx_exec *ex, const HostTag &t, int64_t x0, int64_t nxe, int vl, int part) {
   const int64_t eb = ex->elem_bytes;
   const int64_t epv = (1ll << vl) / eb;  // elements per vector
   DevTag g;
@@ -301,13 +423,14 @@ void add_devtag(ghx_exec *ex, const HostTag &t, int64_t x0, int64_t nxe, int vl,
   g.sz = (uint8_t)fz.s;
   g.vlog = (uint8_t)vl;
   ex->htags.push_back(g);
-  tag_remote.push_back(t.remote ? 1 : 0);
+  ex->hkeys.emplace_back(t.sfab, t.dfab, t.shift[0], t.shift[1], t.shift[2], part, g.nxv, g.ny, g.nz, vl);
+  ex->hremote.push_back(t.remote ? 1 : 0);
 }
 
 // Split a row range into an unaligned head, 16-byte body and tail when src
 // and dst share the same 16-byte phase; otherwise use the widest common
 // vector for the whole row.
-void emit_tag(ghx_exec *ex, const HostTag &t, std::vector<int32_t> &tag_remote) {
+void emit_tag(ghx_exec *ex, const HostTag &t) {
   const int64_t eb = ex->elem_bytes;
   const int64_t xb = t.nx * eb;
   const int64_t ps = (t.s.off * eb) % 16, pd = (t.d.off * eb) % 16;
@@ -317,37 +440,153 @@ void emit_tag(ghx_exec *ex, const HostTag &t, std::vector<int32_t> &tag_remote) 
     const int64_t head = ((16 - ps) % 16) / eb;
     const int64_t body = ((t.nx - head) * eb / 16) * 16 / eb;
     const int64_t tail = t.nx - head - body;
-    if (head > 0) add_devtag(ex, t, 0, head, vec_log(t, eb, 0, head), tag_remote);
-    if (body > 0) add_devtag(ex, t, head, body, 4, tag_remote);
-    if (tail > 0) add_devtag(ex, t, head + body, tail, vec_log(t, eb, head + body, tail), tag_remote);
+    if (head > 0) add_devtag(ex, t, 0, head, vec_log(t, eb, 0, head), 1);
+    if (body > 0) add_devtag(ex, t, head, body, 4, 2);
+    if (tail > 0) add_devtag(ex, t, head + body, tail, vec_log(t, eb, head + body, tail), 3);
     return;
   }
   if (eb < 16 && ps == pd && ps == 0 && strides16 && xb >= 32 && xb % 16 != 0) {
     const int64_t body = (xb / 16) * 16 / eb;
-    add_devtag(ex, t, 0, body, 4, tag_remote);
-    add_devtag(ex, t, body, t.nx - body, vec_log(t, eb, body, t.nx - body), tag_remote);
+    add_devtag(ex, t, 0, body, 4, 2);
+    add_devtag(ex, t, body, t.nx - body, vec_log(t, eb, body, t.nx - body), 3);
     return;
   }
-  add_devtag(ex, t, 0, t.nx, vec_log(t, eb, 0, t.nx), tag_remote);
+  add_devtag(ex, t, 0, t.nx, vec_log(t, eb, 0, t.nx), 0);
 }
 
-void interleave(std::vector<int2> &a, const std::vector<int2> &b) {
-  if (b.empty()) return;
-  if (a.empty()) {
-    a = b;
-    return;
+// Can mirror tags a, b run as a sector swap?  Both 16-byte rows (one vector
+// per row), identical row geometry, and one writes the low half of the
+// 32-byte sector whose high half the other reads (and vice versa).  Returns
+// the index of the tag that writes low halves, or -1.
+int swap_low(const ghx_exec *ex, int ia, int ib) {
+  const DevTag &a = ex->htags[ia], &b = ex->htags[ib];
+  // fab identity (the plan's fab ids); the src and dst pointer slots of one
+  // fab must alias, which ghx_exec_run verifies for swap executors
+  auto fab = [&](int i, bool src) { return src ? std::get<0>(ex->hkeys[i]) : std::get<1>(ex->hkeys[i]); };
+  auto fits = [&](const DevTag &t1, int i1, const DevTag &t2, int i2) {
+    return ex->kind <= GHX_EXEC_LOCAL && t1.vlog == 4 && t2.vlog == 4 && t1.nxv == 1 && t2.nxv == 1 &&
+           t1.ny == t2.ny && t1.nz == t2.nz && t1.nvec == t2.nvec && fab(i1, false) == fab(i2, true) &&
+           fab(i1, true) == fab(i2, false) &&
+           t1.dst_sy == t2.src_sy && t1.dst_sz == t2.src_sz && t1.dst_sc == t2.src_sc &&
+           t1.src_sy == t2.dst_sy && t1.src_sz == t2.dst_sz && t1.src_sc == t2.dst_sc &&
+           t2.src_off == t1.dst_off + 1 && t2.dst_off == t1.src_off + 1 && t1.dst_off % 2 == 0 &&
+           t1.src_off % 2 == 0 && t1.dst_sy % 2 == 0 && t1.dst_sz % 2 == 0 && t1.dst_sc % 2 == 0 &&
+           t1.src_sy % 2 == 0 && t1.src_sz % 2 == 0 && t1.src_sc % 2 == 0;
+  };
+  if (fits(a, ia, b, ib)) return ia;
+  if (fits(b, ib, a, ia)) return ib;
+  return -1;
+}
+
+// Warp tasks.  Mirror tags (src<->dst swapped, opposite shift, same shape)
+// are paired chunk by chunk so the two halves of every shared sector move
+// together; everything else pairs consecutive chunks of one tag.
+void build_tasks(ghx_exec *ex) {
+  const size_t n = ex->htags.size();
+  std::map<PairKey, int32_t> index;
+  for (size_t i = 0; i < n; ++i) index.emplace(ex->hkeys[i], (int32_t)i);
+  std::vector<int32_t> mate(n, -1);
+  const bool pair_mirrors = std::getenv("GHX_NO_MIRROR") == nullptr;
+  if (pair_mirrors)
+    for (size_t i = 0; i < n; ++i) {
+      if (mate[i] >= 0 || ex->hremote[i]) continue;
+      const PairKey &k = ex->hkeys[i];
+      if (std::get<0>(k) == std::get<1>(k) && std::get<2>(k) == 0 && std::get<3>(k) == 0 && std::get<4>(k) == 0)
+        continue;
+      PairKey m(std::get<1>(k), std::get<0>(k), -std::get<2>(k), -std::get<3>(k), -std::get<4>(k), std::get<5>(k),
+                std::get<6>(k), std::get<7>(k), std::get<8>(k), std::get<9>(k));
+      auto it = index.find(m);
+      if (it == index.end() || it->second == (int32_t)i || mate[it->second] >= 0 || ex->hremote[it->second]) continue;
+      mate[i] = it->second;
+      mate[it->second] = (int32_t)i;
+    }
+  std::vector<int4> loc, rem, swaps;
+  ex->npaired = 0;
+  ex->nswap = 0;
+  const bool allow_swap = std::getenv("GHX_NO_SWAP") == nullptr;
+  std::vector<int32_t> swap_lo;  // low tag of every sector-swap pair
+  for (size_t i = 0; i < n; ++i) {
+    const uint32_t nv = ex->htags[i].nvec;
+    auto &out = ex->hremote[i] ? rem : loc;
+    if (mate[i] >= 0) {
+      if ((size_t)mate[i] < i) continue;
+      const int lo = allow_swap ? swap_low(ex, (int)i, mate[i]) : -1;
+      if (lo >= 0) {
+        ex->nswap += 2;
+        const int32_t fa = std::get<0>(ex->hkeys[i]), fb = std::get<1>(ex->hkeys[i]);
+        if (ex->swap_fab.size() <= (size_t)std::max(fa, fb)) ex->swap_fab.resize(std::max(fa, fb) + 1, 0);
+        ex->swap_fab[fa] = ex->swap_fab[fb] = 1;
+        swap_lo.push_back(lo);
+        continue;
+      }
+      ex->npaired += 2;
+      for (uint32_t s = 0; s < nv; s += kChunk) out.push_back(make_int4((int)i, (int)s, mate[i], (int)s));
+    } else {
+      for (uint32_t s = 0; s < nv; s += 2 * kChunk)
+        out.push_back(make_int4((int)i, (int)s, s + kChunk < nv ? (int)i : -1, (int)(s + kChunk)));
+    }
   }
-  std::vector<int2> out;
-  out.reserve(a.size() + b.size());
-  size_t ia = 0, ib = 0;
-  const double ra = 1.0 / a.size(), rb = 1.0 / b.size();
-  while (ia < a.size() || ib < b.size()) {
-    if (ib >= b.size() || (ia < a.size() && (ia + 0.5) * ra <= (ib + 0.5) * rb))
-      out.push_back(a[ia++]);
-    else
-      out.push_back(b[ib++]);
+  // Sector swaps of one chain of fabs (an x-line of boxes: ...L|A|R...) share
+  // 128-byte lines at the row seams (the end of row r and the start of row
+  // r+1 of a fab are adjacent), so the seams of one chain are issued chunk by
+  // chunk together and each line is fetched from / written to HBM once.
+  if (!swap_lo.empty()) {
+    std::map<int32_t, int32_t> parent;
+    std::function<int32_t(int32_t)> find = [&](int32_t x) {
+      auto it = parent.find(x);
+      if (it == parent.end()) {
+        parent[x] = x;
+        return x;
+      }
+      if (it->second == x) return x;
+      const int32_t r = find(it->second);
+      parent[x] = r;
+      return r;
+    };
+    for (int32_t t : swap_lo) {
+      const int32_t a = find(std::get<0>(ex->hkeys[t])), b = find(std::get<1>(ex->hkeys[t]));
+      if (a != b) parent[std::max(a, b)] = std::min(a, b);
+    }
+    std::map<int32_t, std::vector<int32_t>> chains;
+    for (int32_t t : swap_lo) chains[find(std::get<0>(ex->hkeys[t]))].push_back(t);
+    for (auto &kv : chains) {
+      std::vector<int32_t> &ts = kv.second;
+      std::sort(ts.begin(), ts.end());
+      uint32_t maxv = 0;
+      for (int32_t t : ts) maxv = std::max(maxv, ex->htags[t].nvec);
+      for (uint32_t s = 0; s < maxv; s += kChunk)
+        for (int32_t t : ts)
+          if (s < ex->htags[t].nvec) swaps.push_back(make_int4(t, (int)s, -2, -1));
+    }
+    swaps.insert(swaps.end(), loc.begin(), loc.end());
+    loc.swap(swaps);
   }
-  a.swap(out);
+  // proportional interleave of local (HBM) and remote (NVLink) work
+  std::vector<int4> &a = loc;
+  const std::vector<int4> &b = rem;
+  if (!b.empty()) {
+    std::vector<int4> merged;
+    merged.reserve(a.size() + b.size());
+    size_t ia = 0, ib = 0;
+    const double ra = a.empty() ? 0 : 1.0 / a.size(), rb = 1.0 / b.size();
+    while (ia < a.size() || ib < b.size()) {
+      if (ib >= b.size() || (ia < a.size() && (ia + 0.5) * ra <= (ib + 0.5) * rb))
+        merged.push_back(a[ia++]);
+      else
+        merged.push_back(b[ib++]);
+    }
+    a.swap(merged);
+  }
+  ex->htasks.swap(a);
+}
+
+void apply_l2_fetch_limit() {
+  static std::once_flag once;
+  std::call_once(once, []() {
+    const char *v = std::getenv("GHX_L2_FETCH");
+    size_t g = v ? (size_t)std::atoi(v) : 0;
+    if (g == 32 || g == 64 || g == 128) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, g);
+  });
 }
 
 }  // namespace
@@ -381,6 +620,7 @@ int ghx_exec_create(const ghx_plan *plan, int32_t rank, int32_t kind, const int6
   ex->ndst = plan->ndst;
   ex->elem_bytes = elem_bytes;
   ex->nc_loads = plan->mode == GHX_MODE_FILL_BOUNDARY;
+  if (const char *v = std::getenv("GHX_LD_MODE")) ex->ld_mode = std::atoi(v);
   ex->nptrs = (int64_t)plan->nsrc + plan->ndst + 2 * (int64_t)plan->nranks;
   ex->buf_elems.assign(plan->nranks, 0);
 
@@ -396,7 +636,6 @@ int ghx_exec_create(const ghx_plan *plan, int32_t rank, int32_t kind, const int6
   const int32_t send_base = plan->nsrc + plan->ndst;
   const int32_t recv_base = send_base + plan->nranks;
   std::vector<int64_t> buf_off(plan->nranks, 0);
-  std::vector<int32_t> tag_remote;
   int64_t bad = -1;
   for (size_t i = 0; i < plan->wtags.size(); ++i) {
     const Piece &p = plan->wtags[i];
@@ -421,6 +660,9 @@ int ghx_exec_create(const ghx_plan *plan, int32_t rank, int32_t kind, const int6
     t.nz = p.dbox.hi[2] - p.dbox.lo[2] + 1;
     t.nc = ncomp;
     t.remote = p.srank != p.drank;
+    t.sfab = p.src;
+    t.dfab = p.dst;
+    for (int d = 0; d < 3; ++d) t.shift[d] = p.shift[d];
     const bool src_is_fab = kind != GHX_EXEC_UNPACK;
     const bool dst_is_fab = kind != GHX_EXEC_PACK;
     if ((src_is_fab && !contains(S.box, sbox)) || (dst_is_fab && !contains(D.box, p.dbox))) {
@@ -464,7 +706,7 @@ int ghx_exec_create(const ghx_plan *plan, int32_t rank, int32_t kind, const int6
       return GHX_EINVAL;
     }
     ex->elems += cells * ncomp;
-    emit_tag(ex, t, tag_remote);
+    emit_tag(ex, t);
   }
   if (bad >= 0) {
     const Piece &p = plan->wtags[bad];
@@ -475,50 +717,54 @@ int ghx_exec_create(const ghx_plan *plan, int32_t rank, int32_t kind, const int6
     return GHX_EINVAL;
   }
   ex->buf_elems = buf_off;
-  // warp tasks: local and remote streams interleaved so HBM and NVLink work
-  // proceed together in one launch
-  std::vector<int2> loc, rem;
-  for (size_t i = 0; i < ex->htags.size(); ++i) {
-    const uint32_t nv = ex->htags[i].nvec;
-    for (uint32_t s = 0; s < nv; s += kTaskVecs) (tag_remote[i] ? rem : loc).push_back(make_int2((int)i, (int)s));
+  if (ex->htags.size() >= (size_t)INT32_MAX) {
+    set_error("ghx_exec_create: too many tags");
+    delete ex;
+    return GHX_EINVAL;
   }
-  if (ex->htags.size() >= (size_t)INT32_MAX || loc.size() + rem.size() >= (size_t)INT32_MAX) {
+  build_tasks(ex);
+  if (ex->htasks.size() >= (size_t)INT32_MAX / 2) {
     set_error("ghx_exec_create: too many tasks");
     delete ex;
     return GHX_EINVAL;
   }
-  interleave(loc, rem);
-  ex->htasks.swap(loc);
 
-  DeviceGuard g(device);
+  // device tables are uploaded on first run (host-only builds work without a GPU)
+  *out = ex;
+  return GHX_OK;
+}
+
+}  // extern "C"
+
+static int exec_upload(ghx_exec *ex) {
+  if (ex->uploaded) return GHX_OK;
+  apply_l2_fetch_limit();
   cudaError_t e;
   if (!ex->htags.empty()) {
     e = cudaMalloc(&ex->dtags, ex->htags.size() * sizeof(DevTag));
     if (e == cudaSuccess)
       e = cudaMemcpy(ex->dtags, ex->htags.data(), ex->htags.size() * sizeof(DevTag), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMalloc(&ex->dtasks, ex->htasks.size() * sizeof(int2));
+    if (e == cudaSuccess) e = cudaMalloc(&ex->dtasks, ex->htasks.size() * sizeof(int4));
     if (e == cudaSuccess)
-      e = cudaMemcpy(ex->dtasks, ex->htasks.data(), ex->htasks.size() * sizeof(int2), cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) {
-      ghx_exec_free(ex);
-      return cuda_fail(e, "ghx_exec_create: tag upload");
-    }
+      e = cudaMemcpy(ex->dtasks, ex->htasks.data(), ex->htasks.size() * sizeof(int4), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "ghx_exec_run: tag upload");
   }
   e = cudaMalloc(&ex->dptrs, std::max<int64_t>(ex->nptrs, 1) * sizeof(void *));
-  if (e != cudaSuccess) {
-    ghx_exec_free(ex);
-    return cuda_fail(e, "ghx_exec_create: pointer table");
+  if (e != cudaSuccess) return cuda_fail(e, "ghx_exec_run: pointer table");
+  if (ex->blocks == 0) {
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ghx_copy_kernel<0>, kThreads, 0);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ex->device);
+    if (e != cudaSuccess || occ < 1) occ = 1;
+    const int64_t need = ((int64_t)ex->htasks.size() + kWarps - 1) / kWarps;
+    ex->blocks = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)sms * occ));
   }
-  int occ = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ghx_copy_kernel<true>, kThreads, 0);
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  if (e != cudaSuccess || occ < 1) occ = 1;
-  const int64_t need = ((int64_t)ex->htasks.size() + (kThreads / 32) - 1) / (kThreads / 32);
-  ex->blocks = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)sms * occ));
-  *out = ex;
+  ex->uploaded = true;
   return GHX_OK;
 }
+
+extern "C" {
 
 void ghx_exec_free(ghx_exec *ex) {
   if (!ex) return;
@@ -550,6 +796,22 @@ int ghx_exec_info(const ghx_exec *ex, int64_t *ntags, int64_t *ntasks, int64_t *
   return GHX_OK;
 }
 
+int ghx_exec_detail(const ghx_exec *ex, int64_t out[8]) {
+  if (!ex || !out) {
+    set_error("ghx_exec_detail: bad arguments");
+    return GHX_EINVAL;
+  }
+  out[0] = (int64_t)ex->htags.size();
+  out[1] = (int64_t)ex->htasks.size();
+  out[2] = ex->elems;
+  out[3] = 2 * ex->elems * ex->elem_bytes;
+  out[4] = ex->npaired;
+  out[5] = ex->nswap;
+  out[6] = ex->blocks;
+  out[7] = ex->ld_mode;
+  return GHX_OK;
+}
+
 int ghx_exec_buffer_elems(const ghx_exec *ex, int64_t *per_peer) {
   if (!ex || !per_peer) {
     set_error("ghx_exec_buffer_elems: bad arguments");
@@ -567,12 +829,15 @@ int ghx_exec_run(ghx_exec *ex, void *const *ptrs, int64_t nptrs, void *stream) {
   if (ex->htasks.empty()) return GHX_OK;
   std::lock_guard<std::mutex> lk(ex->mu);
   DeviceGuard g(ex->device);
+  if (int rc = exec_upload(ex)) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (ex->cached_ptrs.size() != (size_t)nptrs ||
       std::memcmp(ex->cached_ptrs.data(), ptrs, nptrs * sizeof(void *)) != 0) {
+    const uintptr_t amask = ex->nswap ? 31 : 15;
     for (int64_t i = 0; i < nptrs; ++i)
-      if (reinterpret_cast<uintptr_t>(ptrs[i]) & 15) {
-        set_error("ghx_exec_run: base pointer " + std::to_string(i) + " is not 16-byte aligned");
+      if (reinterpret_cast<uintptr_t>(ptrs[i]) & amask) {
+        set_error("ghx_exec_run: base pointer " + std::to_string(i) + " is not " + std::to_string(amask + 1) +
+                  "-byte aligned");
         return GHX_EINVAL;
       }
     // every slot referenced by this rank's tags must be set
@@ -581,20 +846,37 @@ int ghx_exec_run(ghx_exec *ex, void *const *ptrs, int64_t nptrs, void *stream) {
         set_error("ghx_exec_run: a pointer slot used by this rank's tags is NULL");
         return GHX_EINVAL;
       }
+    // sector swaps read and write both fabs of a pair through one slot each
+    if (ex->nswap)
+      for (int32_t f = 0; f < std::min(ex->nsrc, ex->ndst); ++f)
+        if (ex->swap_fab.size() > (size_t)f && ex->swap_fab[f] && ptrs[f] != ptrs[ex->nsrc + f]) {
+          set_error("ghx_exec_run: FillBoundary executor needs src slot == dst slot for every fab");
+          return GHX_EINVAL;
+        }
     ex->cached_ptrs.assign(ptrs, ptrs + nptrs);
     // pageable source: the copy has consumed the host table when this returns
     cudaError_t e = cudaMemcpyAsync(ex->dptrs, ex->cached_ptrs.data(), nptrs * sizeof(void *),
                                     cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) {
+      const int n = (int)ex->htags.size();
+      ghx_bind_kernel<<<std::min(1184, (n + 255) / 256), 256, 0, st>>>(ex->dtags, n, ex->dptrs);
+      e = cudaGetLastError();
+    }
     if (e != cudaSuccess) {
       ex->cached_ptrs.clear();
-      return cuda_fail(e, "ghx_exec_run: pointer upload");
+      return cuda_fail(e, "ghx_exec_run: pointer bind");
     }
   }
   const int ntasks = (int)ex->htasks.size();
-  if (ex->nc_loads)
-    ghx_copy_kernel<true><<<ex->blocks, ex->threads, 0, st>>>(ex->dtags, ex->dtasks, ntasks, ex->dptrs);
-  else
-    ghx_copy_kernel<false><<<ex->blocks, ex->threads, 0, st>>>(ex->dtags, ex->dtasks, ntasks, ex->dptrs);
+  int ld = ex->ld_mode;
+  if (ld == 0 && !ex->nc_loads) ld = 2;  // sources may alias destinations (ParallelCopy): no .nc
+  switch (ld) {
+    case 0: ghx_copy_kernel<0><<<ex->blocks, ex->threads, 0, st>>>(ex->dtags, ex->dtasks, ntasks); break;
+    case 1: ghx_copy_kernel<1><<<ex->blocks, ex->threads, 0, st>>>(ex->dtags, ex->dtasks, ntasks); break;
+    case 2: ghx_copy_kernel<2><<<ex->blocks, ex->threads, 0, st>>>(ex->dtags, ex->dtasks, ntasks); break;
+    case 3: ghx_copy_kernel<3><<<ex->blocks, ex->threads, 0, st>>>(ex->dtags, ex->dtasks, ntasks); break;
+    default: ghx_copy_kernel<4><<<ex->blocks, ex->threads, 0, st>>>(ex->dtags, ex->dtasks, ntasks); break;
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "ghx_exec_run: launch");
   g_launches.fetch_add(1);

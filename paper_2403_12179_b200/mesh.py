@@ -458,10 +458,12 @@ class MultiFab:
         comm.parallel_copy(self, src, scomp, dcomp, ncomp, ngrow_src, ngrow_dst, geom, backend)
 
     # -- synthetic data (bench / parity tests)
-    def fill_hash(self, seed: int, domain: Box, stream=None) -> None:
-        """Valid cells <- splitmix64 counter hash over ``domain`` (see
-        oracle/inputs.py for the formula), other cells <- sNaN poison."""
-        dom = np.ascontiguousarray(np.asarray(domain.as_row(), np.int64))
+    def fill_hash(self, seed: int, domain, stream=None) -> None:
+        """Valid cells <- splitmix64 counter hash over ``domain`` (a Box or
+        a padded [lo0 lo1 lo2 hi0 hi1 hi2] row; formula in oracle/inputs.py),
+        other cells <- sNaN poison."""
+        row = domain.as_row() if isinstance(domain, Box) else list(domain)
+        dom = np.ascontiguousarray(np.asarray(row, np.int64))
         st = None if stream is None else C.c_void_p(stream)
         for i in self.local_indices:
             f = self.fabs[i]

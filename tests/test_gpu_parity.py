@@ -40,7 +40,7 @@ def test_fill_boundary_matches_reference_golden(name):
     ba = amr.BoxArray(_boxes(amr, c["boxes"], dim, c["nodal"]))
     dm = amr.DistributionMapping(c["rank_of"], c["nranks"])
     geom = amr.Geometry(_domain(amr, c), [0.0] * dim, [1.0] * dim, c["periodic"][:dim])
-    hdom = _domain(amr, c, "hash_domain")
+    hdom = list(c["hash_domain"][0]) + list(c["hash_domain"][1])  # padded 3-D row
     ng = c["ngrow"][:dim]
 
     def program(ctx):

@@ -58,6 +58,10 @@ constexpr int kChunk = 32 * kU;     // vectors per chunk (a task has two)
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kSwapSlots = 8;
+constexpr int kChainRows = 64;  // rows per chain task
+#ifndef GHX_CHAIN_R
+#define GHX_CHAIN_R 2
+#endif
 
 std::atomic<int64_t> g_launches{0};
 
@@ -203,28 +207,81 @@ __device__ __forceinline__ void store_chunk(const DevTag &t, uint32_t start, int
 // (SL.lo, SA.hi): each lane reads two whole sectors and writes them back
 // whole, so L2 never refills a partially written sector from HBM.
 template <int LD>
-__device__ __noinline__ void swap_chunk(const DevTag &t, uint32_t start, int lane) {
+__device__ __forceinline__ void swap_chunk(const DevTag &t, uint32_t start, int lane) {
   constexpr int kS = kU / 2;
   char *const da = reinterpret_cast<char *>(t.dst);
   char *const sl = reinterpret_cast<char *>(t.src);
-#pragma unroll
+#pragma unroll 1
   for (int h = 0; h < 2; ++h) {
-    u8x32 a[kS], l[kS];
+    uint4 lo[kS], hi[kS];
 #pragma unroll
     for (int u = 0; u < kS; ++u) {
       const uint32_t v = start + (uint32_t)((h * kS + u) * 32 + lane);
       if (v < t.nvec) {
-        a[u] = ld32<LD>(da + (vec_offset<false>(t, v) << 4));
-        l[u] = ld32<LD>(sl + (vec_offset<true>(t, v) << 4));
+        hi[u] = ld16<LD>(da + (vec_offset<false>(t, v) << 4) + 16);
+        lo[u] = ld16<LD>(sl + (vec_offset<true>(t, v) << 4));
       }
     }
 #pragma unroll
     for (int u = 0; u < kS; ++u) {
       const uint32_t v = start + (uint32_t)((h * kS + u) * 32 + lane);
       if (v < t.nvec) {
-        const uint32_t w[8] = {l[u].w[0], l[u].w[1], l[u].w[2], l[u].w[3], a[u].w[4], a[u].w[5], a[u].w[6], a[u].w[7]};
+        const uint32_t w[8] = {lo[u].x, lo[u].y, lo[u].z, lo[u].w, hi[u].x, hi[u].y, hi[u].z, hi[u].w};
         st32(da + (vec_offset<false>(t, v) << 4), w);
         st32(sl + (vec_offset<true>(t, v) << 4), w);
+      }
+    }
+  }
+}
+
+// A chain task runs the sector swaps of every seam of one chain of fabs
+// (e.g. the x-line L|A|R|... of a uniform decomposition) over the same rows
+// in one warp: lane = (seam j, row offset).  Row r+1 of seam (L,A) and row r
+// of seam (A,R) touch the two halves of the same 64 bytes of A (end of row
+// r, start of row r+1), so their loads coalesce into one line request.
+template <int LD>
+__device__ __forceinline__ void chain_task(const DevTag *__restrict__ tags, const int *__restrict__ chain,
+                                           int off, int k, uint32_t start, uint32_t rows, int lane) {
+  const int per = 32 / k;
+  const int j = lane / per;
+  const int rl = lane - j * per;
+  if (j >= k) return;
+  const DevTag &t = tags[__ldg(chain + off + j)];
+  char *const da = reinterpret_cast<char *>(__ldg(&t.dst));
+  char *const sl = reinterpret_cast<char *>(__ldg(&t.src));
+  const uint32_t nvec = __ldg(&t.nvec), ny = __ldg(&t.ny), nz = __ldg(&t.nz);
+  const uint32_t my = __ldg(&t.my), mz = __ldg(&t.mz);
+  const uint32_t shy = __ldg(&t.sy), shz = __ldg(&t.sz);
+  const int64_t dsy = __ldg(&t.dst_sy), dsz = __ldg(&t.dst_sz), dsc = __ldg(&t.dst_sc);
+  const int64_t ssy = __ldg(&t.src_sy), ssz = __ldg(&t.src_sz), ssc = __ldg(&t.src_sc);
+  const uint32_t end = min(nvec, start + rows);
+  constexpr int R = GHX_CHAIN_R;  // rows per lane per iteration (2R loads in flight)
+  // only the halves that survive are loaded: the new content of both
+  // sectors is (L-sector low half | A-sector high half)
+#pragma unroll 1
+  for (uint32_t r0 = start + rl; r0 < end; r0 += R * per) {
+    uint4 lo[R], hi[R];
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      const uint32_t r = r0 + u * per;
+      if (r < end) {
+        const uint32_t q = fdiv(r, ny, my, shy);
+        const uint32_t c = fdiv(q, nz, mz, shz);
+        const uint32_t y = r - q * ny, z = q - c * nz;
+        hi[u] = ld16<LD>(da + (((int64_t)y * dsy + (int64_t)z * dsz + (int64_t)c * dsc) << 4) + 16);
+        lo[u] = ld16<LD>(sl + (((int64_t)y * ssy + (int64_t)z * ssz + (int64_t)c * ssc) << 4));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      const uint32_t r = r0 + u * per;
+      if (r < end) {
+        const uint32_t q = fdiv(r, ny, my, shy);
+        const uint32_t c = fdiv(q, nz, mz, shz);
+        const uint32_t y = r - q * ny, z = q - c * nz;
+        const uint32_t w[8] = {lo[u].x, lo[u].y, lo[u].z, lo[u].w, hi[u].x, hi[u].y, hi[u].z, hi[u].w};
+        st32(da + (((int64_t)y * dsy + (int64_t)z * dsz + (int64_t)c * dsc) << 4), w);
+        st32(sl + (((int64_t)y * ssy + (int64_t)z * ssz + (int64_t)c * ssc) << 4), w);
       }
     }
   }
@@ -248,57 +305,79 @@ __global__ void ghx_bind_kernel(DevTag *tags, int ntags, void *const *__restrict
 }
 
 // tasks: {tagA, startA, tagB (-1: none), startB}
+// Dynamic schedule: warps grab batches of kBatch consecutive tasks from a
+// per-executor counter (counter[0]); every warp counts itself out in
+// counter[1] and the last one resets both, so the next launch (stream
+// ordered) starts from zero without a memset.  Heavy tasks come first.
 template <int LD>
 __global__ void __launch_bounds__(kThreads) ghx_copy_kernel(const DevTag *__restrict__ tags,
-                                                            const int4 *__restrict__ tasks, int ntasks) {
+                                                            const int4 *__restrict__ tasks, int ntasks,
+                                                            const int *__restrict__ chains,
+                                                            unsigned long long *__restrict__ counter, int batch) {
   __shared__ DevTag slots[kWarps][2];
   __shared__ DevTag swc[kWarps][kSwapSlots];  // direct-mapped cache of sector-swap descriptors
   __shared__ int swc_id[kWarps][kSwapSlots];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int first = (int)(warp * ntasks / nwarps);
-  const int last = (int)((warp + 1) * ntasks / nwarps);
   DevTag &ta = slots[wib][0];
   DevTag &tb = slots[wib][1];
   int have_a = -1, have_b = -1;
   if (lane < kSwapSlots) swc_id[wib][lane] = -1;
   __syncwarp();
-  int4 tk = first < last ? __ldg(tasks + first) : make_int4(0, 0, -1, 0);
-  for (int w = first; w < last; ++w) {
-    const int4 nxt = (w + 1 < last) ? __ldg(tasks + w + 1) : tk;  // prefetch
-    if (tk.z == -2) {  // sector-swap task over one chunk of T1
-      const int sl = tk.x & (kSwapSlots - 1);
-      if (swc_id[wib][sl] != tk.x) {
-        __syncwarp();
-        fetch_tag(tags, tk.x, &swc[wib][sl], lane);
-        if (lane == 0) swc_id[wib][sl] = tk.x;
-        __syncwarp();
-      }
-      swap_chunk<LD>(swc[wib][sl], (uint32_t)tk.y, lane);
-      if (tk.w >= 0) swap_chunk<LD>(swc[wib][sl], (uint32_t)tk.w, lane);
-      tk = nxt;
-      continue;
-    }
-    if (tk.x != have_a || tk.z != have_b) {
-      __syncwarp();
-      if (tk.x == have_b && tk.z == have_a) {  // swapped pair order: swap roles
-        tk = make_int4(tk.z, tk.w, tk.x, tk.y);
+  unsigned long long nb = 0;
+  if (lane == 0) nb = atomicAdd(counter, (unsigned long long)batch);
+  nb = __shfl_sync(0xffffffffu, nb, 0);
+#pragma unroll 1
+  while (true) {
+    const long long first = (long long)nb;
+    if (first >= ntasks) break;
+    if (lane == 0) nb = atomicAdd(counter, (unsigned long long)batch);  // prefetch the next batch
+    const int last = (int)min((long long)ntasks, first + batch);
+    int4 tk = __ldg(tasks + first);
+#pragma unroll 1
+    for (int w = (int)first; w < last; ++w) {
+      const int4 nxt = (w + 1 < last) ? __ldg(tasks + w + 1) : tk;
+      if (tk.z == -3) {  // chain task: all seams of one chain, kChainRows rows
+        chain_task<LD>(tags, chains, tk.x, tk.w, (uint32_t)tk.y, kChainRows, lane);
+      } else if (tk.z == -2) {  // sector-swap task over one chunk of T1
+        const int sl = tk.x & (kSwapSlots - 1);
+        if (swc_id[wib][sl] != tk.x) {
+          __syncwarp();
+          fetch_tag(tags, tk.x, &swc[wib][sl], lane);
+          if (lane == 0) swc_id[wib][sl] = tk.x;
+          __syncwarp();
+        }
+        swap_chunk<LD>(swc[wib][sl], (uint32_t)tk.y, lane);
+        if (tk.w >= 0) swap_chunk<LD>(swc[wib][sl], (uint32_t)tk.w, lane);
       } else {
-        if (tk.x != have_a) fetch_tag(tags, tk.x, &ta, lane);
-        if (tk.z >= 0 && tk.z != have_b) fetch_tag(tags, tk.z, &tb, lane);
-        have_a = tk.x;
-        have_b = tk.z;
+        if (tk.x != have_a || tk.z != have_b) {
+          __syncwarp();
+          if (tk.x == have_b && tk.z == have_a) {  // swapped pair order: swap roles
+            tk = make_int4(tk.z, tk.w, tk.x, tk.y);
+          } else {
+            if (tk.x != have_a) fetch_tag(tags, tk.x, &ta, lane);
+            if (tk.z >= 0 && tk.z != have_b) fetch_tag(tags, tk.z, &tb, lane);
+            have_a = tk.x;
+            have_b = tk.z;
+          }
+          __syncwarp();
+        }
+        uint4 va[kU], vb[kU];
+        load_chunk<LD>(ta, (uint32_t)tk.y, lane, va);
+        if (tk.z >= 0) load_chunk<LD>(tb, (uint32_t)tk.w, lane, vb);
+        store_chunk(ta, (uint32_t)tk.y, lane, va);
+        if (tk.z >= 0) store_chunk(tb, (uint32_t)tk.w, lane, vb);
       }
-      __syncwarp();
+      tk = nxt;
     }
-    uint4 va[kU], vb[kU];
-    load_chunk<LD>(ta, (uint32_t)tk.y, lane, va);
-    if (tk.z >= 0) load_chunk<LD>(tb, (uint32_t)tk.w, lane, vb);
-    store_chunk(ta, (uint32_t)tk.y, lane, va);
-    if (tk.z >= 0) store_chunk(tb, (uint32_t)tk.w, lane, vb);
-    tk = nxt;
+    nb = __shfl_sync(0xffffffffu, nb, 0);
+  }
+  if (lane == 0) {
+    const unsigned long long total = (unsigned long long)gridDim.x * (blockDim.x >> 5);
+    if (atomicAdd(counter + 1, 1ull) == total - 1) {
+      counter[0] = 0;
+      counter[1] = 0;
+    }
   }
 }
 
@@ -383,6 +462,9 @@ struct ghx_exec {
   std::vector<PairKey> hkeys;
   std::vector<int32_t> hremote;
   std::vector<int4> htasks;
+  std::vector<int> hchain;  // chain tables (tag indices of consecutive seams)
+  int *dchain = nullptr;
+  unsigned long long *dcounter = nullptr;
   DevTag *dtags = nullptr;
   int4 *dtasks = nullptr;
   void **dptrs = nullptr;
@@ -549,17 +631,38 @@ void build_tasks(ghx_exec *ex) {
     }
     std::map<int32_t, std::vector<int32_t>> chains;
     for (int32_t t : swap_lo) chains[find(std::get<0>(ex->hkeys[t]))].push_back(t);
+    const bool chain_tasks = std::getenv("GHX_NO_CHAIN") == nullptr;
     for (auto &kv : chains) {
       std::vector<int32_t> &ts = kv.second;
       std::sort(ts.begin(), ts.end());
+      bool uniform = chain_tasks && ts.size() <= 32;
+      for (int32_t t : ts) uniform = uniform && ex->htags[t].nvec == ex->htags[ts[0]].nvec;
+      if (uniform) {
+        const int off = (int)ex->hchain.size();
+        ex->hchain.insert(ex->hchain.end(), ts.begin(), ts.end());
+        for (uint32_t s = 0; s < ex->htags[ts[0]].nvec; s += kChainRows)
+          swaps.push_back(make_int4(off, (int)s, -3, (int)ts.size()));
+        continue;
+      }
       uint32_t maxv = 0;
       for (int32_t t : ts) maxv = std::max(maxv, ex->htags[t].nvec);
       for (uint32_t s = 0; s < maxv; s += kChunk)
         for (int32_t t : ts)
           if (s < ex->htags[t].nvec) swaps.push_back(make_int4(t, (int)s, -2, -1));
     }
-    swaps.insert(swaps.end(), loc.begin(), loc.end());
-    loc.swap(swaps);
+    // spread the latency-bound seam work over the launch so it overlaps the
+    // bandwidth-bound row copies
+    std::vector<int4> merged;
+    merged.reserve(swaps.size() + loc.size());
+    size_t ia = 0, ib = 0;
+    const double ra = 1.0 / swaps.size(), rb = loc.empty() ? 0 : 1.0 / loc.size();
+    while (ia < swaps.size() || ib < loc.size()) {
+      if (ib >= loc.size() || (ia < swaps.size() && (ia + 0.5) * ra <= (ib + 0.5) * rb))
+        merged.push_back(swaps[ia++]);
+      else
+        merged.push_back(loc[ib++]);
+    }
+    loc.swap(merged);
   }
   // proportional interleave of local (HBM) and remote (NVLink) work
   std::vector<int4> &a = loc;
@@ -744,6 +847,11 @@ static int exec_upload(ghx_exec *ex) {
     e = cudaMalloc(&ex->dtags, ex->htags.size() * sizeof(DevTag));
     if (e == cudaSuccess)
       e = cudaMemcpy(ex->dtags, ex->htags.data(), ex->htags.size() * sizeof(DevTag), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&ex->dcounter, 2 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemset(ex->dcounter, 0, 2 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMalloc(&ex->dchain, std::max<size_t>(1, ex->hchain.size()) * sizeof(int));
+    if (e == cudaSuccess && !ex->hchain.empty())
+      e = cudaMemcpy(ex->dchain, ex->hchain.data(), ex->hchain.size() * sizeof(int), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&ex->dtasks, ex->htasks.size() * sizeof(int4));
     if (e == cudaSuccess)
       e = cudaMemcpy(ex->dtasks, ex->htasks.data(), ex->htasks.size() * sizeof(int4), cudaMemcpyHostToDevice);
@@ -759,6 +867,7 @@ static int exec_upload(ghx_exec *ex) {
     if (e != cudaSuccess || occ < 1) occ = 1;
     const int64_t need = ((int64_t)ex->htasks.size() + kWarps - 1) / kWarps;
     ex->blocks = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)sms * occ));
+    if (const char *v = std::getenv("GHX_BLOCKS")) ex->blocks = std::max(1, std::atoi(v));
   }
   ex->uploaded = true;
   return GHX_OK;
@@ -771,6 +880,8 @@ void ghx_exec_free(ghx_exec *ex) {
   DeviceGuard g(ex->device);
   if (ex->dtags) cudaFree(ex->dtags);
   if (ex->dtasks) cudaFree(ex->dtasks);
+  if (ex->dchain) cudaFree(ex->dchain);
+  if (ex->dcounter) cudaFree(ex->dcounter);
   if (ex->dptrs) cudaFree(ex->dptrs);
   delete ex;
 }
@@ -868,14 +979,16 @@ int ghx_exec_run(ghx_exec *ex, void *const *ptrs, int64_t nptrs, void *stream) {
     }
   }
   const int ntasks = (int)ex->htasks.size();
+  // tasks per atomic grab: ~8 grabs per warp, at least 1, at most 64
+  const int batch = (int)std::max<int64_t>(1, std::min<int64_t>(64, ntasks / ((int64_t)ex->blocks * kWarps * 8)));
   int ld = ex->ld_mode;
   if (ld == 0 && !ex->nc_loads) ld = 2;  // sources may alias destinations (ParallelCopy): no .nc
   switch (ld) {
-    case 0: ghx_copy_kernel<0><<<ex->blocks, ex->threads, 0, st>>>(ex->dtags, ex->dtasks, ntasks); break;
-    case 1: ghx_copy_kernel<1><<<ex->blocks, ex->threads, 0, st>>>(ex->dtags, ex->dtasks, ntasks); break;
-    case 2: ghx_copy_kernel<2><<<ex->blocks, ex->threads, 0, st>>>(ex->dtags, ex->dtasks, ntasks); break;
-    case 3: ghx_copy_kernel<3><<<ex->blocks, ex->threads, 0, st>>>(ex->dtags, ex->dtasks, ntasks); break;
-    default: ghx_copy_kernel<4><<<ex->blocks, ex->threads, 0, st>>>(ex->dtags, ex->dtasks, ntasks); break;
+    case 0: ghx_copy_kernel<0><<<ex->blocks, ex->threads, 0, st>>>(ex->dtags, ex->dtasks, ntasks, ex->dchain, ex->dcounter, batch); break;
+    case 1: ghx_copy_kernel<1><<<ex->blocks, ex->threads, 0, st>>>(ex->dtags, ex->dtasks, ntasks, ex->dchain, ex->dcounter, batch); break;
+    case 2: ghx_copy_kernel<2><<<ex->blocks, ex->threads, 0, st>>>(ex->dtags, ex->dtasks, ntasks, ex->dchain, ex->dcounter, batch); break;
+    case 3: ghx_copy_kernel<3><<<ex->blocks, ex->threads, 0, st>>>(ex->dtags, ex->dtasks, ntasks, ex->dchain, ex->dcounter, batch); break;
+    default: ghx_copy_kernel<4><<<ex->blocks, ex->threads, 0, st>>>(ex->dtags, ex->dtasks, ntasks, ex->dchain, ex->dcounter, batch); break;
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "ghx_exec_run: launch");

@@ -652,17 +652,22 @@ void build_tasks(ghx_exec *ex) {
     }
     // spread the latency-bound seam work over the launch so it overlaps the
     // bandwidth-bound row copies
+    if (std::getenv("GHX_NO_INTERLEAVE")) {
+      swaps.insert(swaps.end(), loc.begin(), loc.end());
+      loc.swap(swaps);
+      swaps.clear();
+    }
     std::vector<int4> merged;
     merged.reserve(swaps.size() + loc.size());
     size_t ia = 0, ib = 0;
     const double ra = 1.0 / swaps.size(), rb = loc.empty() ? 0 : 1.0 / loc.size();
-    while (ia < swaps.size() || ib < loc.size()) {
+    while (!swaps.empty() && (ia < swaps.size() || ib < loc.size())) {
       if (ib >= loc.size() || (ia < swaps.size() && (ia + 0.5) * ra <= (ib + 0.5) * rb))
         merged.push_back(swaps[ia++]);
       else
         merged.push_back(loc[ib++]);
     }
-    loc.swap(merged);
+    if (!swaps.empty()) loc.swap(merged);
   }
   // proportional interleave of local (HBM) and remote (NVLink) work
   std::vector<int4> &a = loc;
@@ -980,7 +985,10 @@ int ghx_exec_run(ghx_exec *ex, void *const *ptrs, int64_t nptrs, void *stream) {
   }
   const int ntasks = (int)ex->htasks.size();
   // tasks per atomic grab: ~8 grabs per warp, at least 1, at most 64
-  const int batch = (int)std::max<int64_t>(1, std::min<int64_t>(64, ntasks / ((int64_t)ex->blocks * kWarps * 8)));
+  // tasks per atomic grab: small batches balance best (measured), large task
+  // lists amortise the atomic
+  int batch = (int)std::max<int64_t>(2, std::min<int64_t>(64, ntasks / ((int64_t)ex->blocks * kWarps * 16)));
+  if (const char *v = std::getenv("GHX_BATCH")) batch = std::max(1, std::atoi(v));
   int ld = ex->ld_mode;
   if (ld == 0 && !ex->nc_loads) ld = 2;  // sources may alias destinations (ParallelCopy): no .nc
   switch (ld) {

@@ -12,6 +12,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <vector>
+#include <cstring>
 
 #define CK(x)                                                                       \
   do {                                                                              \
@@ -173,6 +174,37 @@ int main() {
     const int64_t n = nrows * ROW / 16;
     float ms = timeit([&] { copy_dense<<<sms * 8, 256>>>((const uint4 *)buf, (uint4 *)buf2, n); }, 5);
     printf("dense copy:                               %.3f ms  %.1f GB/s (r+w)\n", ms, 2.0 * n * 16 / ms / 1e6);
+  }
+  // pinned host memory (zero-copy over PCIe)
+  {
+    const int64_t hrows = (1ll << 30) / ROW;  // 1 GiB
+    char *h;
+    CK(cudaHostAlloc(&h, hrows * ROW, cudaHostAllocMapped));
+    memset(h, 1, hrows * ROW);
+    char *hd;
+    CK(cudaHostGetDevicePointer(&hd, h, 0));
+    for (int64_t off : {0, 1024}) {
+      float ms = timeit([&] { rd_sector<<<sms * 16, 256>>>(hd, hrows, off, sink, 1); }, 3);
+      printf("HOST read isolated 32B sector off=%ld: %.3f ms  %.2f GB/s useful\n", (long)off, ms, hrows * 32.0 / ms / 1e6);
+    }
+    {
+      float ms = timeit([&] { rd_sector<<<sms * 16, 256>>>(hd, hrows, 0, sink, 3); }, 3);
+      printf("HOST read isolated 16B: %.3f ms  %.2f GB/s useful\n", ms, hrows * 16.0 / ms / 1e6);
+    }
+    {
+      float ms = timeit([&] { rw_sector<<<sms * 16, 256>>>(hd, hrows, 0); }, 3);
+      printf("HOST read+write isolated 32B sector: %.3f ms  %.2f GB/s useful (64B/row)\n", ms, hrows * 64.0 / ms / 1e6);
+    }
+    {
+      const int64_t n = hrows * ROW / 16;
+      float ms = timeit([&] { copy_dense<<<sms * 8, 256>>>((const uint4 *)hd, (uint4 *)buf2, n); }, 3);
+      printf("HOST->DEV dense read: %.3f ms  %.2f GB/s\n", ms, n * 16.0 / ms / 1e6);
+      ms = timeit([&] { copy_dense<<<sms * 8, 256>>>((const uint4 *)buf2, (uint4 *)hd, n); }, 3);
+      printf("DEV->HOST dense write: %.3f ms  %.2f GB/s\n", ms, n * 16.0 / ms / 1e6);
+      ms = timeit([&] { cudaMemcpyAsync(buf2, h, n * 16, cudaMemcpyHostToDevice); }, 3);
+      printf("cudaMemcpy H2D: %.3f ms  %.2f GB/s\n", ms, n * 16.0 / ms / 1e6);
+    }
+    cudaFreeHost(h);
   }
   // TMA
   PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;

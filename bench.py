@@ -41,7 +41,7 @@ SEED = 20261017
 CONFIGS = {
     "C1": dict(kind="fb", n=64, box=32, ncomp=1, ngrow=1,
                desc="C1: 64^3 periodic domain, 32^3 boxes, ncomp 1, nghost 1, float64 FillBoundary"),
-    "C2": dict(kind="fb", n=256, box=64, ncomp=4, ngrow=2,
+    "C2": dict(kind="fb", n=256, box=64, ncomp=4, ngrow=2, weak=True,
                desc="C2: 256^3 periodic domain, 64^3 boxes, ncomp 4, nghost 2, float64 FillBoundary"),
     "C3": dict(kind="fb", n=512, box=128, ncomp=8, ngrow=2,
                desc="C3: 512^3 periodic domain, 128^3 boxes, ncomp 8, nghost 2, float64 FillBoundary"),
@@ -81,10 +81,29 @@ def ncu_traffic(cfg_name):
 
 # ----------------------------------------------------------------- layout
 
+WEAK_FACTORS = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2), 16: (4, 2, 2)}
+
+
+def scaled(cfg, world):
+    """The default workload is BASELINE.json configs[1] (C2) at N=1 and the
+    same per-GPU work at N GPUs (weak scaling: the 256^3 domain repeated
+    N times, 64^3 boxes round-robin).  Other configs are fixed-size (strong)."""
+    cfg = dict(cfg)
+    ext = (cfg["n"],) * 3
+    if cfg.get("weak") and world > 1:
+        f = WEAK_FACTORS.get(world)
+        if f is None:
+            raise SystemExit(f"weak-scaled workload defined for N in {sorted(WEAK_FACTORS)}")
+        ext = tuple(cfg["n"] * k for k in f)
+        cfg["desc"] += f" -- weak-scaled to {ext[0]}x{ext[1]}x{ext[2]} over {world} GPUs ({cfg['n']}^3 per GPU)"
+    cfg["ext"] = ext
+    return cfg
+
+
 def layout(amr, cfg, G):
     amr.config.set_spacedim(3)
-    n = cfg["n"]
-    dom = amr.Box((0, 0, 0), (n - 1,) * 3)
+    ext = cfg.get("ext", (cfg["n"],) * 3)
+    dom = amr.Box((0, 0, 0), tuple(e - 1 for e in ext))
     geom = amr.Geometry(dom, (0.0,) * 3, (1.0,) * 3, (True,) * 3)
     ba = amr.decompose(dom, cfg["box"])
     dm = amr.DistributionMapping.round_robin(len(ba), G)
@@ -296,8 +315,8 @@ def run_reference(args, cfg, rank, world):
     line = {
         "metric": METRIC, "impl": "reference", "value": round(value, 4), "unit": "GB/s",
         "n_gpus": args.gpus, "steps": len(t), "warmup": W, "ms_per_step": round(1e3 * total / len(t), 4),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (uninitialised values; pure copy)",
+        "higher_is_better": True, "scaling": "weak" if cfg.get("weak") else "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (uninitialised values; pure copy)",
         "config": {"workload": cfg["desc"], "sample": desc},
         "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": workers, "kind": "port",
                          "sample": desc, "cpu_model": cpu_model(), "os_cpu_count": os.cpu_count()},
@@ -384,7 +403,7 @@ def run_ours(args, cfg, rank, world):
         "warmup": args.warmup, "ms_per_step": round(mean_ms_max, 5), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (splitmix64 counter-hash valid cells, sNaN-poisoned ghosts)",
-        "config": {"workload": cfg["desc"], "domain": cfg["n"], "box": cfg["box"], "ncomp": cfg["ncomp"],
+        "config": {"workload": cfg["desc"], "domain": list(cfg["ext"]), "box": cfg["box"], "ncomp": cfg["ncomp"],
                    "nghost": cfg["ngrow"], "boxes": len(L["ba"]), "segments": plan.num_segments,
                    "ghost_bytes_per_step": ghost_bytes, "parallelism": f"boxes round-robin over {world} GPU(s)",
                    "transport": x.transport if world > 1 else "local",
@@ -461,7 +480,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS),
+                    help="default C2 = BASELINE.json configs[1] (the 1-B200 config), weak-scaled for N>1")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--transport", default=None, choices=["p2p", "nccl"])
     ap.add_argument("--e2e-steps", type=int, default=10)
@@ -475,12 +495,12 @@ def main():
         args.warmup = 3
     if args.transport:
         os.environ["GHX_TRANSPORT"] = args.transport
-    cfg = dict(CONFIGS[args.config])
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    cfg = scaled(CONFIGS[args.config], world)
     if args.ngrow:
         g = tuple(int(v) for v in args.ngrow.split(","))
         cfg["ngrow"] = g if len(g) == 3 else g[0]
         cfg["desc"] += f" [diagnostic ngrow={args.ngrow}]"
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)

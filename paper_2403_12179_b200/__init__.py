@@ -20,3 +20,5 @@ from .mesh import (BoxArray, DistributionMapping, Fab, FabView, MultiFab, decomp
                    fab_setval, multifab_define, storage_shape)
 
 __version__ = "0.1.0"
+from .bridge import BoundArray4, MfiAccessor, array_view, multifab_iter  # noqa: E402
+from .comm import prepare_fill_boundary, prepare_parallel_copy  # noqa: E402

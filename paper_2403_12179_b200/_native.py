@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libghostx.so")
+# GHX_LIB: developer override (kernel-variant experiments, scripts/variants.sh)
+LIB_PATH = os.environ.get("GHX_LIB") or os.path.join(_HERE, "_lib", "libghostx.so")
 
 GHX_OK, GHX_EINVAL, GHX_ECUDA, GHX_ENOMEM, GHX_EOVERLAP = 0, 1, 2, 3, 4
 MODE_FILL_BOUNDARY, MODE_PARALLEL_COPY = 0, 1

@@ -53,7 +53,13 @@ using ghx::set_error;
 
 namespace {
 
-constexpr int kU = 4;               // vectors per lane per chunk
+#ifndef GHX_KU
+#define GHX_KU 4
+#endif
+#ifndef GHX_MINB
+#define GHX_MINB 1
+#endif
+constexpr int kU = GHX_KU;          // vectors per lane per chunk
 constexpr int kChunk = 32 * kU;     // vectors per chunk (a task has two)
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
@@ -310,7 +316,7 @@ __global__ void ghx_bind_kernel(DevTag *tags, int ntags, void *const *__restrict
 // counter[1] and the last one resets both, so the next launch (stream
 // ordered) starts from zero without a memset.  Heavy tasks come first.
 template <int LD>
-__global__ void __launch_bounds__(kThreads) ghx_copy_kernel(const DevTag *__restrict__ tags,
+__global__ void __launch_bounds__(kThreads, GHX_MINB) ghx_copy_kernel(const DevTag *__restrict__ tags,
                                                             const int4 *__restrict__ tasks, int ntasks,
                                                             const int *__restrict__ chains,
                                                             unsigned long long *__restrict__ counter, int batch) {

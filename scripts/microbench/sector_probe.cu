@@ -65,6 +65,27 @@ __global__ void rw_sector(char *buf, int64_t nrows, int64_t off) {
   }
 }
 
+__global__ void wr_sector(char *buf, int64_t nrows, int64_t off, int mode) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrows; r += (int64_t)gridDim.x * blockDim.x) {
+    char *p = buf + r * ROW + off;
+    const uint32_t v = (uint32_t)r;
+    if (mode == 0)
+      asm volatile("st.global.v8.u32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"l"(p), "r"(v) : "memory");
+    else if (mode == 1)
+      asm volatile("st.global.wt.v8.u32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"l"(p), "r"(v) : "memory");
+    else if (mode == 2)
+      asm volatile("st.global.cs.v8.u32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"l"(p), "r"(v) : "memory");
+    else if (mode == 3)
+      asm volatile("st.global.v4.u32 [%0], {%1,%1,%1,%1};" ::"l"(p), "r"(v) : "memory");
+    else if (mode == 4) {  // full 128-byte line (8 x 16B from 8 consecutive... one lane writes 4 x 32B)
+      char *q = buf + r * 128;
+      for (int i = 0; i < 4; ++i)
+        asm volatile("st.global.v8.u32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"l"(q + 32 * i), "r"(v) : "memory");
+    } else if (mode == 5)
+      asm volatile("st.global.L1::no_allocate.v8.u32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"l"(p), "r"(v) : "memory");
+  }
+}
+
 __global__ void copy_dense(const uint4 *a, uint4 *b, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     b[i] = a[i];
@@ -194,6 +215,14 @@ int main() {
     {
       float ms = timeit([&] { rw_sector<<<sms * 16, 256>>>(hd, hrows, 0); }, 3);
       printf("HOST read+write isolated 32B sector: %.3f ms  %.2f GB/s useful (64B/row)\n", ms, hrows * 64.0 / ms / 1e6);
+    }
+    const char *wn[] = {"st.v8", "st.wt.v8", "st.cs.v8", "st.v4 (16B)", "full 128B lines (contiguous)", "st.na.v8"};
+    for (int m = 0; m < 6; ++m) {
+      const int64_t rows = m == 4 ? (hrows * ROW / 128) : hrows;
+      float ms = timeit([&] { wr_sector<<<sms * 16, 256>>>(hd, rows, 0, m); }, 3);
+      const double useful = m == 4 ? 128.0 : (m == 3 ? 16.0 : 32.0);
+      printf("HOST write isolated %-28s: %.3f ms  %.2f GB/s useful  %.3f G writes/s\n", wn[m], ms,
+             rows * useful / ms / 1e6, rows / ms / 1e6);
     }
     {
       const int64_t n = hrows * ROW / 16;

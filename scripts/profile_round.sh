@@ -1,0 +1,28 @@
+#!/usr/bin/env bash
+# Profiling pass on one GPU (run under gpurun from the repo root):
+#   ncu launch list of the headline bench command (C3), one --set full capture
+#   of ghx_copy_kernel, per-config DRAM traffic, and the bench lines.
+mkdir -p gpurun_out/prof
+export PYTHONDONTWRITEBYTECODE=1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file gpurun_out/prof/launches_C2.csv python bench.py --config C2 --steps 5 --warmup 3 --no-e2e --no-cpu \
+  > gpurun_out/prof/launches_C2.log 2>&1
+echo "launch list rc=$?"
+for c in C2 C3; do
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:ghx_copy_kernel -s 4 -c 1 -f \
+    -o gpurun_out/prof/full_$c python bench.py --config $c --steps 3 --warmup 3 --no-e2e --no-cpu \
+    > gpurun_out/prof/full_$c.log 2>&1
+  echo "full $c rc=$?"
+done
+for c in C1 C2 C3 C4 C5; do
+  timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sectors_srcunit_tex_op_read.sum,lts__t_sectors_srcunit_tex_op_write.sum,sm__warps_active.avg.pct_of_peak_sustained_active \
+    --clock-control none --csv -k regex:ghx_copy_kernel -s 4 -c 1 python bench.py --config $c --steps 3 --warmup 3 --no-e2e --no-cpu \
+    > gpurun_out/prof/traffic_$c.csv 2> gpurun_out/prof/traffic_$c.err
+  echo "traffic $c rc=$?"
+done
+for c in C1 C2 C3 C4 C5; do
+  timeout 900 python bench.py --config $c --steps ${BENCH_STEPS:-200} --warmup 5 > gpurun_out/prof/bench_$c.json 2> gpurun_out/prof/bench_$c.log
+  echo "bench $c rc=$?"
+done
+timeout 600 python bench.py --impl reference --steps 20 --warmup 3 > gpurun_out/prof/bench_ref_C2.json 2> gpurun_out/prof/bench_ref_C2.log
+echo "bench ref rc=$?"

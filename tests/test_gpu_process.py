@@ -1,0 +1,89 @@
+"""Process-per-GPU exchange path on one GPU: two processes (gloo process
+group for the plumbing) share cuda:0, map each other's fab slabs with CUDA
+IPC and push remote tags straight into the peer's ghost cells (host-side
+synchronisation, since both ranks share the device).  Checked against the
+wrapped-hash property and the reference's per-pair message accounting."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+import golden_util as gu
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, q, n, b, nc, ng):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                          WORLD_SIZE=str(world), LOCAL_RANK="0")
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import paper_2403_12179_b200 as amr
+        from gpu_util import device_bits, expected_wrapped
+        from oracle import inputs
+        amr.config.set_spacedim(3)
+        dom = amr.Box((0, 0, 0), (n - 1,) * 3)
+        geom = amr.Geometry(dom, (0.0,) * 3, (1.0,) * 3, (True,) * 3)
+        ba = amr.decompose(dom, b)
+        dm = amr.DistributionMapping.round_robin(len(ba), world)
+        mf = amr.MultiFab(ba, dm, nc, ng, geom)
+        mf.fill_hash(inputs.SEED, dom)
+        torch.cuda.synchronize()
+        ctx = amr.current_ctx()
+        s0 = ctx.bus.stats_snapshot()
+        amr.fill_boundary(mf, geom)
+        amr.fill_boundary(mf, geom)
+        s1 = ctx.bus.stats_snapshot()
+        bad = 0
+        for gi in mf.local_indices:
+            f = mf.fabs[gi]
+            exp = expected_wrapped(f, nc, dom.as_row(), (1, 1, 1), inputs.SEED, 8)
+            bad += int((device_bits(f) != exp).sum().item())
+        stats = {f"{s}->{d}": (s1[(s, d)][0] - s0[(s, d)][0], s1[(s, d)][1] - s0[(s, d)][1])
+                 for (s, d) in s1 if s1[(s, d)] != s0[(s, d)]}
+        dist.barrier()
+        del mf
+        dist.destroy_process_group()
+        q.put((rank, (bad, stats)))
+    except BaseException:  # noqa: BLE001
+        import traceback
+        q.put((rank, "ERROR " + traceback.format_exc()))
+
+
+@pytest.mark.parametrize("cfg", [("C1", 64, 32, 1, 1, "C1_x2"), ("C3", 512, 128, 8, 2, "C3_x2")])
+def test_two_processes_one_gpu_ipc_push(cfg):
+    name, n, b, nc, ng, golden = cfg
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, n, b, nc, ng)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+    for r in range(world):
+        assert not isinstance(res[r], str), res[r]
+        assert res[r][0] == 0, f"rank {r}: {res[r][0]} cells differ"
+    c = gu.case(golden)
+    pair_bytes = {}
+    for r in range(world):
+        for k, (msgs, nbytes) in res[r][1].items():
+            assert msgs == 2  # two calls, one message per ordered pair per call
+            pair_bytes[k] = nbytes // 2
+    assert pair_bytes == {k: v * nc // c["ncomp"] for k, v in c["pair_bytes"].items()}

@@ -158,7 +158,7 @@ class ClockSampler:
 
     def __init__(self, device, period=0.01):
         self.ok = False
-        self.samples, self.reasons = [], set()
+        self.samples, self.reasons, self.mem_samples = [], set(), []
         try:
             import pynvml
             pynvml.nvmlInit()
@@ -191,6 +191,7 @@ class ClockSampler:
         while not self._stop.is_set():
             try:
                 self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.mem_samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_MEM))
                 r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 for bit, name in self.REASONS.items():
                     if r & bit and bit != 0x1:
@@ -215,6 +216,7 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": getattr(self, "max_mhz", None), "reasons": sorted(self.reasons),
                     "samples": len(self.samples)}
         return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "mem_mhz": statistics.median(self.mem_samples) if self.mem_samples else None,
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
@@ -383,6 +385,19 @@ def run_ours(args, cfg, rank, world):
             C.c_uint64(SEED), 8, None))
         verified = bool(torch.equal(flat, exp))
     hbm_peak, peak_src = peaks()
+    # context only: this box's device-to-device copy rate right now (2 GiB,
+    # best of 3); the roofline denominator stays MEASURED_PEAKS.json
+    big = torch.empty(1 << 30, dtype=torch.int16, device=dev)
+    big2 = torch.empty_like(big)
+    best = 0.0
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        big2.copy_(big)
+        e1.record()
+        e1.synchronize()
+        best = max(best, 2 * big.numel() * 2 / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+    del big, big2
     alg = x.ex.alg_bytes if x.transport == "p2p" else None
     roof = None
     if alg is not None:
@@ -391,7 +406,7 @@ def run_ours(args, cfg, rank, world):
                 "frac": round(achieved / hbm_peak, 4),
                 "traffic": ncu_traffic(args.config) if world == 1 else None,
                 "kernel": "ghx_copy_kernel", "algorithmic_bytes_per_launch": int(alg),
-                "peak_source": peak_src}
+                "peak_source": peak_src, "box_copy_gbs_now": round(best, 1)}
         if world > 1:
             rb = x.remote_cells * x.ncomp * x.item
             roof["nvlink"] = {"bytes_per_launch_out": int(rb),

@@ -352,13 +352,20 @@ def run_ours(args, cfg, rank, world):
         dist.barrier()
     torch.cuda.synchronize()
     l0 = N.lib.ghx_launch_count()
+    can_enqueue = x.mode == "serial" or x.transport == "nccl" or x.sync == "device"
     with ClockSampler(dev) as clk:
         for i in range(K):
             flush.zero_()
             ev0[i].record(stream)
-            x.enqueue(stream.cuda_stream)
+            if can_enqueue:
+                x.enqueue(stream.cuda_stream)
+            else:  # ranks sharing one GPU: host-synchronised exchange
+                x.run()
             ev1[i].record(stream)
         torch.cuda.synchronize()
+    if x.mode == "process" and x.sync == "device":
+        from paper_2403_12179_b200 import comm as _comm
+        _comm.check_barriers()
     launches = N.lib.ghx_launch_count() - l0
     if dist:
         dist.barrier()
@@ -422,6 +429,7 @@ def run_ours(args, cfg, rank, world):
                    "nghost": cfg["ngrow"], "boxes": len(L["ba"]), "segments": plan.num_segments,
                    "ghost_bytes_per_step": ghost_bytes, "parallelism": f"boxes round-robin over {world} GPU(s)",
                    "transport": x.transport if world > 1 else "local",
+                   "sync": x.sync if world > 1 else None,
                    "l2": "flushed before every step (512 MiB write, outside the events)",
                    "tags_this_rank": x.ex.ntags if x.transport == "p2p" else None,
                    "warp_tasks_this_rank": x.ex.ntasks if x.transport == "p2p" else None,
@@ -524,7 +532,11 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
     if world > 1:
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", torch.cuda.current_device()))
+        backend = os.environ.get("GHX_BENCH_BACKEND", "nccl")  # gloo: ranks sharing one GPU (tests)
+        if backend == "nccl":
+            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", torch.cuda.current_device()))
+        else:
+            torch.distributed.init_process_group(backend)
     try:
         run_ours(args, cfg, rank, world)
     finally:

@@ -147,6 +147,10 @@ int ghx_stream_sync(void *stream);
  * flag array (nranks uint64) as mapped in this process. */
 int ghx_signal_barrier(uint64_t *const *flag_ptrs, int32_t rank, int32_t nranks, uint64_t epoch,
                        void *stream);
+/* Number of device barriers (this process, current device) that gave up
+ * after GHX_BARRIER_TIMEOUT_S seconds (default 30) instead of hanging;
+ * synchronous read, -1 on error. */
+int64_t ghx_barrier_timeouts(void);
 
 /* Synthetic input generator (bench / tests): valid cells of the fab get
  * splitmix64(seed ^ lin(i,j,k,c)) mapped to [0,1) (see oracle/inputs.py),

@@ -61,6 +61,7 @@ _SIGS = {
     "ghx_ipc_close_handle": (C.c_int, [P]),
     "ghx_stream_sync": (C.c_int, [P]),
     "ghx_signal_barrier": (C.c_int, [C.POINTER(P), I32, I32, C.c_uint64, P]),
+    "ghx_barrier_timeouts": (I64, []),
     "ghx_fill_hash": (C.c_int, [P, PI64, I32, PI64, PI64, C.c_uint64, I32, P]),
     "ghx_fill_hash_wrapped": (C.c_int, [P, PI64, I32, PI64, PI32, C.c_uint64, I32, P]),
     "ghx_launch_count": (I64, []),

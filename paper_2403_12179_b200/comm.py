@@ -752,8 +752,23 @@ class Exchange:
         self.t_local = _table(self.local, src_mf, own, bufs)
 
     def _enqueue_nccl(self, stream: int) -> None:
+        import torch
         import torch.distributed as dist
         self.pack.run(self.t_pack, stream)
+        if dist.get_backend() != "nccl":
+            # host-staged message passing (gloo): test path for ranks sharing a GPU
+            torch.cuda.current_stream(self.device).synchronize()
+            send = {r: t.cpu() for r, t in self.send_t.items()}
+            recv = {r: torch.empty(t.shape, dtype=t.dtype) for r, t in self.recv_t.items()}
+            ops = [dist.P2POp(dist.isend, t, r) for r, t in sorted(send.items())]
+            ops += [dist.P2POp(dist.irecv, t, r) for r, t in sorted(recv.items())]
+            for q in (dist.batch_isend_irecv(ops) if ops else []):
+                q.wait()
+            for r, t in recv.items():
+                self.recv_t[r].copy_(t)
+            self.local.run(self.t_local, stream)
+            self.unpack.run(self.t_unpack, stream)
+            return
         ops = [dist.P2POp(dist.isend, t, r) for r, t in sorted(self.send_t.items())]
         ops += [dist.P2POp(dist.irecv, t, r) for r, t in sorted(self.recv_t.items())]
         reqs = dist.batch_isend_irecv(ops) if ops else []
@@ -801,8 +816,23 @@ class Exchange:
         else:
             self.enqueue(stream.cuda_stream)
             stream.synchronize()
+            if self.mode == "process" and self.sync == "device":
+                check_barriers()
         for (s, d, nbytes) in self.messages:
             ctx.bus.account(s, d, nbytes)
+
+
+_barrier_timeouts_seen = 0
+
+
+def check_barriers() -> None:
+    """Raise if a device barrier timed out (a peer rank never arrived)."""
+    global _barrier_timeouts_seen
+    n = int(N.lib.ghx_barrier_timeouts())
+    if n > _barrier_timeouts_seen:
+        _barrier_timeouts_seen = n
+        raise N.GhostxError("device barrier timed out: a peer rank did not arrive "
+                            "(GHX_BARRIER_TIMEOUT_S); the exchange result is incomplete")
 
 
 def exchange_for(plan: CommPlan, src_mf: MultiFab, dst_mf: MultiFab, scomp: int, dcomp: int, ncomp: int,

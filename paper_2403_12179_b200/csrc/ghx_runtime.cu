@@ -4,6 +4,7 @@
 // can address local fabs, peer-mapped fabs and IPC-mapped fabs uniformly.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -40,7 +41,17 @@ struct FlagPtrs {
   uint64_t *p[64];
 };
 
-__global__ void barrier_kernel(FlagPtrs flags, int rank, int nranks, uint64_t epoch) {
+__device__ unsigned int g_barrier_timeouts = 0;
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Spins at most timeout_ns: a peer that never arrives (crashed rank) makes
+// the barrier give up and count a timeout instead of hanging the GPU.
+__global__ void barrier_kernel(FlagPtrs flags, int rank, int nranks, uint64_t epoch, uint64_t timeout_ns) {
   const int peer = threadIdx.x;
   if (peer >= nranks) return;
   // make every earlier write of this stream visible system-wide, then signal
@@ -48,10 +59,17 @@ __global__ void barrier_kernel(FlagPtrs flags, int rank, int nranks, uint64_t ep
   uint64_t *remote = flags.p[peer] + rank;
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(remote), "l"(epoch) : "memory");
   const uint64_t *mine = flags.p[rank] + peer;
+  const uint64_t t0 = globaltimer_ns();
   uint64_t v = 0;
-  do {
+  for (uint32_t it = 0;; ++it) {
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine) : "memory");
-  } while (v < epoch);
+    if (v >= epoch) break;
+    if ((it & 1023) == 1023 && globaltimer_ns() - t0 > timeout_ns) {
+      atomicAdd(&g_barrier_timeouts, 1u);
+      break;
+    }
+    __nanosleep(64);
+  }
 }
 
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
@@ -261,7 +279,12 @@ int ghx_signal_barrier(uint64_t *const *flag_ptrs, int32_t rank, int32_t nranks,
     }
     f.p[i] = flag_ptrs[i];
   }
-  barrier_kernel<<<1, 64, 0, (cudaStream_t)stream>>>(f, rank, nranks, epoch);
+  static const uint64_t timeout_ns = [] {
+    const char *v = std::getenv("GHX_BARRIER_TIMEOUT_S");
+    const double sec = v ? std::atof(v) : 30.0;
+    return (uint64_t)(sec * 1e9);
+  }();
+  barrier_kernel<<<1, 64, 0, (cudaStream_t)stream>>>(f, rank, nranks, epoch, timeout_ns);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(e, "ghx_signal_barrier");
   return GHX_OK;
@@ -297,6 +320,12 @@ static int fill_hash(void *fab, const int64_t fab_box[6], int32_t ncomp, const i
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(e, "ghx_fill_hash");
   return GHX_OK;
+}
+
+int64_t ghx_barrier_timeouts(void) {
+  unsigned int v = 0;
+  if (cudaMemcpyFromSymbol(&v, g_barrier_timeouts, sizeof(v)) != cudaSuccess) return -1;
+  return (int64_t)v;
 }
 
 int ghx_fill_hash(void *fab, const int64_t fab_box[6], int32_t ncomp, const int64_t valid_box[6],

@@ -24,10 +24,11 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, q, n, b, nc, ng):
+def _worker(rank, world, port, q, n, b, nc, ng, env=None):
     try:
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
                           WORLD_SIZE=str(world), LOCAL_RANK="0")
+        os.environ.update(env or {})
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(0)
@@ -64,14 +65,22 @@ def _worker(rank, world, port, q, n, b, nc, ng):
         q.put((rank, "ERROR " + traceback.format_exc()))
 
 
-@pytest.mark.parametrize("cfg", [("C1", 64, 32, 1, 1, "C1_x2"), ("C3", 512, 128, 8, 2, "C3_x2")])
-def test_two_processes_one_gpu_ipc_push(cfg):
-    name, n, b, nc, ng, golden = cfg
+CASES = [("C1", 64, 32, 1, 1, "C1_x2", {}), ("C3", 512, 128, 8, 2, "C3_x2", {}),
+         # device flag barriers between two processes time-sliced on one GPU
+         ("C1", 64, 32, 1, 1, "C1_x2", {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "20"}),
+         # the pack -> message -> unpack fallback (host-staged over gloo here)
+         ("C1", 64, 32, 1, 1, "C1_x2", {"GHX_TRANSPORT": "nccl"}),
+         ("C3", 512, 128, 8, 2, "C3_x2", {"GHX_TRANSPORT": "nccl"})]
+
+
+@pytest.mark.parametrize("cfg", CASES, ids=["C1-ipc", "C3-ipc", "C1-ipc-devbarrier", "C1-fallback", "C3-fallback"])
+def test_two_processes_one_gpu(cfg):
+    name, n, b, nc, ng, golden, env = cfg
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q, n, b, nc, ng)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, n, b, nc, ng, env)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=600) for _ in range(world))

@@ -415,6 +415,8 @@ def run_ours(args, cfg, rank, world):
                 "kernel": "ghx_copy_kernel", "algorithmic_bytes_per_launch": int(alg),
                 "peak_source": peak_src, "box_copy_gbs_now": round(best, 1)}
         if world > 1:
+            launches_note = x.launches_per_call
+            roof["launches_per_step"] = launches_note
             rb = x.remote_cells * x.ncomp * x.item
             roof["nvlink"] = {"bytes_per_launch_out": int(rb),
                               "achieved": round(rb / (mean_ms * 1e-3) / 1e9, 2),
@@ -430,6 +432,7 @@ def run_ours(args, cfg, rank, world):
                    "ghost_bytes_per_step": ghost_bytes, "parallelism": f"boxes round-robin over {world} GPU(s)",
                    "transport": x.transport if world > 1 else "local",
                    "sync": x.sync if world > 1 else None,
+                   "remote": x.remote if world > 1 else None,
                    "l2": "flushed before every step (512 MiB write, outside the events)",
                    "tags_this_rank": x.ex.ntags if x.transport == "p2p" else None,
                    "warp_tasks_this_rank": x.ex.ntasks if x.transport == "p2p" else None,

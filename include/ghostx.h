@@ -48,6 +48,12 @@ extern "C" {
 #define GHX_EXEC_LOCAL 1  /* only tags whose src and dst rank are this rank   */
 #define GHX_EXEC_PACK 2   /* remote tags of this rank -> per-peer send buffer */
 #define GHX_EXEC_UNPACK 3 /* per-peer recv buffer -> remote tags into my fabs */
+/* packed push: local tags + wide-row remote tags stored into peer fabs +
+ * narrow-row remote tags (row bytes <= GHX_PACK_ROW_BYTES, default 128)
+ * packed contiguously into the per-peer send slot (= the peer's mapped
+ * receive buffer); the receiver then runs GHX_EXEC_UNPACK_PACKED. */
+#define GHX_EXEC_PUSH_PACKED 4
+#define GHX_EXEC_UNPACK_PACKED 5
 
 typedef struct ghx_plan ghx_plan;
 typedef struct ghx_exec ghx_exec;

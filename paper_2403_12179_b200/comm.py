@@ -701,8 +701,13 @@ class Exchange:
             self.sync = _sync_mode(ctx) if self.transport == "p2p" else "stream"
         else:
             self.sync = "host" if self.mode == "thread" else "none"
+        self.remote = "direct"
+        self.unp = None
         if self.transport == "nccl":
             self._init_nccl()
+        elif self.mode == "process" and os.environ.get("GHX_REMOTE", "packed") == "packed":
+            self.remote = "packed"
+            self._init_packed()
         else:
             self.ex = plan.executor(me, N.EXEC_DIRECT, src_mf, dst_mf, scomp, dcomp, ncomp)
             if self.mode == "serial":
@@ -720,6 +725,48 @@ class Exchange:
         self.local_cells = int(row[me])
         self.remote_cells = int(sum(row[d] for d in range(plan.nranks) if d != me))
         self.ghost_bytes = int(plan.pair_cells.sum()) * ncomp * self.item  # whole job, counted once
+
+    # -- packed push (process mode) ---------------------------------------
+    def _init_packed(self):
+        """Narrow-row remote tags are packed by the sending kernel straight
+        into the receiver's CUDA-IPC-mapped receive slab (contiguous NVLink
+        stores); the receiver unpacks locally after the exit barrier.  Wide
+        rows, and all local tags, are stored directly into the fabs."""
+        plan, src_mf, dst_mf, ctx, me = self.plan, self.src, self.dst, self.ctx, self.ctx.rank
+        a = (self.scomp, self.dcomp, self.ncomp)
+        self.ex = plan.executor(me, N.EXEC_PUSH_PACKED, src_mf, dst_mf, *a)
+        self.unp = plan.executor(me, N.EXEC_UNPACK_PACKED, src_mf, dst_mf, *a)
+        item, n = self.item, plan.nranks
+        recv_el = self.unp.buffer_elems
+        offs, total = [], 0
+        for r in range(n):
+            offs.append(total)
+            total += -(-int(recv_el[r]) * item // 256) * 256
+        self._recv = Slab(max(256, total), dst_mf.device)
+        h = (C.c_uint8 * 64)()
+        N.check(N.lib.ghx_ipc_get_handle(C.c_void_p(self._recv.ptr), h))
+        infos = ctx.allgather((me, bytes(h), offs, self.ex.buffer_elems.tolist(), recv_el.tolist()))
+        for (s_, _, _, send_el, _) in infos:
+            for (d_, _, _, _, rcv) in infos:
+                if s_ != d_ and send_el[d_] != rcv[s_]:
+                    raise RuntimeError(f"packed-push buffer mismatch {s_}->{d_}: {send_el[d_]} vs {rcv[s_]}")
+        send = np.zeros(n, np.uint64)
+        self._opened = []
+        for (r, hb, roffs, _, _) in infos:
+            if r == me or self.ex.buffer_elems[r] == 0:
+                continue
+            p = C.c_void_p()
+            N.check(N.lib.ghx_ipc_open_handle(dst_mf.device, (C.c_uint8 * 64).from_buffer_copy(hb), C.byref(p)))
+            self._opened.append(p.value)
+            send[r] = p.value + roffs[me]
+        recv = np.asarray([self._recv.ptr + o for o in offs], np.uint64)
+        bufs = np.concatenate([send, recv])
+        parts = _ipc_peers(ctx, dst_mf)
+        self.table = _table(self.ex, src_mf, parts, bufs)
+        self.t_unp = _table(self.unp, src_mf, [(dst_mf.local_indices, dst_mf._ptrs)], bufs)
+        weakref.finalize(self, _close_ipc, list(self._opened))
+        if self.sync == "device":
+            self.psync = _process_sync(ctx)
 
     # -- NCCL fallback ---------------------------------------------------
     def _init_nccl(self):
@@ -780,7 +827,7 @@ class Exchange:
     # -- launching ---------------------------------------------------------
     @property
     def launches_per_call(self) -> int:
-        return 3 if self.transport == "nccl" else 1
+        return 3 if self.transport == "nccl" else (2 if self.remote == "packed" else 1)
 
     def enqueue(self, stream: int) -> None:
         if self.transport == "nccl":
@@ -791,6 +838,8 @@ class Exchange:
             self.psync.barrier(stream)  # peers finished earlier work on their fabs
             self.ex.run(self.table, stream)
             self.psync.barrier(stream)  # every push into my fabs has landed
+            if self.unp is not None:
+                self.unp.run(self.t_unp, stream)
         else:
             raise RuntimeError(f"{self.mode} ranks with host synchronisation cannot enqueue; use run()")
 
@@ -813,6 +862,9 @@ class Exchange:
             self.ex.run(self.table, stream.cuda_stream)
             stream.synchronize()
             ctx.barrier()
+            if self.unp is not None:
+                self.unp.run(self.t_unp, stream.cuda_stream)
+                stream.synchronize()
         else:
             self.enqueue(stream.cuda_stream)
             stream.synchronize()

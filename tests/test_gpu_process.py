@@ -65,7 +65,8 @@ def _worker(rank, world, port, q, n, b, nc, ng, env=None):
         q.put((rank, "ERROR " + traceback.format_exc()))
 
 
-CASES = [("C1", 64, 32, 1, 1, "C1_x2", {}), ("C3", 512, 128, 8, 2, "C3_x2", {}),
+CASES = [("C1", 64, 32, 1, 1, "C1_x2", {"GHX_REMOTE": "direct"}), ("C3", 512, 128, 8, 2, "C3_x2", {}),
+         ("C3", 512, 128, 8, 2, "C3_x2", {"GHX_REMOTE": "direct"}),
          # device flag barriers between two processes time-sliced on one GPU
          ("C1", 64, 32, 1, 1, "C1_x2", {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "20"}),
          # the pack -> message -> unpack fallback (host-staged over gloo here)
@@ -73,7 +74,8 @@ CASES = [("C1", 64, 32, 1, 1, "C1_x2", {}), ("C3", 512, 128, 8, 2, "C3_x2", {}),
          ("C3", 512, 128, 8, 2, "C3_x2", {"GHX_TRANSPORT": "nccl"})]
 
 
-@pytest.mark.parametrize("cfg", CASES, ids=["C1-ipc", "C3-ipc", "C1-ipc-devbarrier", "C1-fallback", "C3-fallback"])
+@pytest.mark.parametrize("cfg", CASES, ids=["C1-ipc-direct", "C3-ipc-packed", "C3-ipc-direct", "C1-devbarrier-packed",
+                                            "C1-fallback", "C3-fallback"])
 def test_two_processes_one_gpu(cfg):
     name, n, b, nc, ng, golden, env = cfg
     world = 2

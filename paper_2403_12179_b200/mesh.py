@@ -163,124 +163,112 @@ def fab_create(box: Box, ncomp: int, arena=None) -> Fab:
     return Fab(box, ncomp, arena)
 
 
-def _comp_slice(comp_range, ncomp: int) -> slice:
-    if comp_range is None:
-        return slice(0, ncomp)
-    if isinstance(comp_range, int):
-        if not 0 <= comp_range < ncomp:
-            raise ValueError(f"component {comp_range} out of range [0,{ncomp})")
-        return slice(comp_range, comp_range + 1)
-    a, b = comp_range
-    if not 0 <= a <= b <= ncomp:
-        raise ValueError(f"component range {comp_range} out of range [0,{ncomp}]")
-    return slice(a, b)
+def _components(spec, ncomp: int) -> slice:
+    """None -> all, int c -> [c, c+1), (a, b) -> [a, b); ValueError outside."""
+    if spec is None:
+        lo, hi = 0, ncomp
+    elif isinstance(spec, (int, np.integer)):
+        lo, hi = int(spec), int(spec) + 1
+        if hi > ncomp or lo < 0:
+            raise ValueError(f"component {spec} does not exist (ncomp={ncomp})")
+    else:
+        lo, hi = (int(v) for v in spec)
+        if lo < 0 or hi < lo or hi > ncomp:
+            raise ValueError(f"component range {tuple(spec)} not within [0, {ncomp}]")
+    return slice(lo, hi)
 
 
 def _region_slices(fab_box: Box, region: Box) -> tuple:
-    lo, rlo, rhi = _pad3(fab_box.lo, 0), _pad3(region.lo, 0), _pad3(region.hi, 0)
-    return tuple(slice(b - a, c - a + 1) for a, b, c in zip(lo, rlo, rhi))
+    """Zero-based (x, y, z) slices of ``region`` inside a fab over ``fab_box``."""
+    base = _pad3(fab_box.lo, 0)
+    lo, hi = _pad3(region.lo, 0), _pad3(region.hi, 0)
+    return tuple(slice(l - o, h - o + 1) for o, l, h in zip(base, lo, hi))
 
 
 def fab_setval(f: Fab, value: float, region: Box | None = None, comp_range=None) -> None:
-    region = f.box if region is None else region
-    if region.is_empty:
+    """Assign ``value`` to region x comps of the fab (whole fab by default)."""
+    target = f.box if region is None else region
+    if target.is_empty:
         return
-    if not f.box.contains(region):
-        raise ValueError(f"setval region {region} is not contained in fab box {f.box}")
-    sx, sy, sz = _region_slices(f.box, region)
-    f.data[sx, sy, sz, _comp_slice(comp_range, f.ncomp)] = value
+    if not f.box.contains(target):
+        raise ValueError(f"setval: {target} lies outside the fab box {f.box}")
+    f.data[_region_slices(f.box, target) + (_components(comp_range, f.ncomp),)] = value
 
 
 class FabView:
-    """Globally indexed accessor over a fab's (nx, ny, nz, ncomp) tensor.
-
-    Index with ints (returns a Python float) or integer arrays (returns a
-    tensor), as view[i, j, k], view[i, j, k, c] or in spacedim arity."""
+    """Global-index accessor of a fab: view[i, j, k], view[i, j, k, c] or
+    spacedim-arity indices; ints give a Python float, integer arrays give a
+    tensor (fancy indexing, evaluated on the fab's device)."""
 
     __slots__ = ("_a", "lo3", "ncomp", "writable")
 
     def __init__(self, data, lo3: tuple, ncomp: int, writable: bool):
-        self._a = data
-        self.lo3 = lo3
-        self.ncomp = ncomp
-        self.writable = writable
+        self._a, self.lo3, self.ncomp, self.writable = data, lo3, ncomp, writable
 
     @property
     def array(self):
         return self._a
 
-    def _locate(self, idx):
-        torch = _torch()
-        if not isinstance(idx, tuple):
-            idx = (idx,)
-        n = len(idx)
-        if n == 4:
-            spatial, comp = idx[:3], idx[3]
-        elif n == 3:
-            spatial, comp = idx, 0
-        elif n == config.spacedim:
-            spatial, comp = tuple(idx) + (0,) * (3 - n), 0
+    def _resolve(self, key):
+        key = key if isinstance(key, tuple) else (key,)
+        if len(key) == 4:
+            pos, comp = key[:3], key[3]
+        elif len(key) == 3 or len(key) == config.spacedim:
+            pos, comp = tuple(key) + (0,) * (3 - len(key)), 0
         else:
-            raise IndexError(f"expected (i,j,k[,c]) indices, got {n} entries")
-        out = []
+            raise IndexError(f"FabView takes (i, j, k[, c]) or {config.spacedim} indices, got {len(key)}")
         scalar = isinstance(comp, (int, np.integer))
-        for d, v in enumerate(spatial):
-            if isinstance(v, (int, np.integer)):
-                li = int(v) - self.lo3[d]
-                if li < 0 or li >= self._a.shape[d]:
-                    raise IndexError(f"index {v} out of bounds on axis {d}")
-                out.append(li)
+        loc = []
+        for axis, (g, base) in enumerate(zip(pos, self.lo3)):
+            if isinstance(g, (int, np.integer)):
+                z = int(g) - base
+                if not 0 <= z < self._a.shape[axis]:
+                    raise IndexError(f"index {g} outside the fab on axis {axis}")
+                loc.append(z)
             else:
                 scalar = False
-                t = torch.as_tensor(np.asarray(v) - self.lo3[d], device=self._a.device)
-                out.append(t)
-        out.append(comp)
-        return tuple(out), scalar
+                loc.append(_torch().as_tensor(np.asarray(g) - base, device=self._a.device))
+        return tuple(loc) + (comp,), scalar
 
-    def __getitem__(self, idx):
-        loc, scalar = self._locate(idx)
-        v = self._a[loc]
-        return v.item() if scalar else v
+    def __getitem__(self, key):
+        loc, scalar = self._resolve(key)
+        out = self._a[loc]
+        return out.item() if scalar else out
 
-    def __setitem__(self, idx, value):
+    def __setitem__(self, key, value):
         if not self.writable:
-            raise ValueError("assignment through a read-only FabView")
-        loc, _ = self._locate(idx)
-        torch = _torch()
+            raise ValueError("this FabView is read-only")
+        loc, _ = self._resolve(key)
         if isinstance(value, np.ndarray):
-            value = torch.as_tensor(value, device=self._a.device, dtype=self._a.dtype)
+            value = _torch().as_tensor(value, device=self._a.device, dtype=self._a.dtype)
         self._a[loc] = value
 
 
 class BoxArray:
-    """Ordered, pairwise-disjoint valid boxes of one index type."""
+    """Pairwise-disjoint valid boxes (one centering), in a fixed order.  The
+    disjointness check is the native binned sweep ``ghx_boxes_disjoint``."""
 
     def __init__(self, boxes: Iterable[Box], ixtype=None):
-        boxes = tuple(boxes)
+        self.boxes = tuple(boxes)
         self.uid = _next_uid()
-        if not boxes:
-            self.boxes = boxes
-            self.ixtype = ixtype if ixtype is not None else IndexType.cell()
+        self._grown = {}
+        if not self.boxes:
+            self.ixtype = IndexType.cell() if ixtype is None else ixtype
             self._rows = np.zeros((0, 6), np.int64)
             self._dim = config.spacedim
             return
-        t = boxes[0].ixtype
-        for b in boxes:
-            if b.is_empty:
-                raise ValueError("BoxArray boxes must be non-empty")
-            if b.ixtype != t:
-                raise ValueError("BoxArray boxes must share one index type")
-        rows = np.ascontiguousarray(np.array([b.as_row() for b in boxes], dtype=np.int64))
-        oa, ob = C.c_int64(), C.c_int64()
-        N.check(N.lib.ghx_boxes_disjoint(len(boxes), N.i64p(rows), C.byref(oa), C.byref(ob)))
-        if oa.value >= 0:
-            raise ValueError(f"BoxArray valid regions must be disjoint: {boxes[oa.value]} and "
-                             f"{boxes[ob.value]} overlap")
-        self.boxes = boxes
-        self.ixtype = t
-        self._rows = rows
-        self._dim = len(boxes[0].lo)
-        self._grown = {}
+        self.ixtype = self.boxes[0].ixtype
+        if any(b.is_empty for b in self.boxes):
+            raise ValueError("BoxArray: empty boxes are not allowed")
+        if any(b.ixtype != self.ixtype for b in self.boxes):
+            raise ValueError("BoxArray: all boxes need the same index type")
+        self._rows = np.ascontiguousarray(np.array([b.as_row() for b in self.boxes], dtype=np.int64))
+        self._dim = len(self.boxes[0].lo)
+        first, second = C.c_int64(), C.c_int64()
+        N.check(N.lib.ghx_boxes_disjoint(len(self.boxes), N.i64p(self._rows), C.byref(first), C.byref(second)))
+        if first.value >= 0:
+            raise ValueError(f"BoxArray: valid regions must be disjoint, but {self.boxes[first.value]} "
+                             f"overlaps {self.boxes[second.value]}")
 
     def __len__(self) -> int:
         return len(self.boxes)
@@ -292,52 +280,53 @@ class BoxArray:
         return iter(self.boxes)
 
     def minimal_extent(self) -> int:
-        r = self._rows
-        return int((r[:, 3:3 + self._dim] - r[:, :self._dim] + 1).min())
+        d = self._dim
+        return int((self._rows[:, 3:3 + d] - self._rows[:, :d]).min()) + 1
 
     def rows(self, ngrow=None) -> np.ndarray:
-        """(n, 6) int64 lo/hi rows padded to 3 axes, optionally grown."""
+        """(n, 6) int64 [lo0 lo1 lo2 hi0 hi1 hi2] rows, optionally grown."""
         if ngrow is None:
             return self._rows
         g = _pad3(ngrow, 0)
-        out = self._grown.get(g)
-        if out is None:
-            out = self._rows.copy()
-            out[:, :3] -= np.asarray(g, np.int64)
-            out[:, 3:] += np.asarray(g, np.int64)
-            out = np.ascontiguousarray(out)
-            self._grown[g] = out
-        return out
+        if g not in self._grown:
+            grown = self._rows.copy()
+            grown[:, :3] -= g
+            grown[:, 3:] += g
+            self._grown[g] = np.ascontiguousarray(grown)
+        return self._grown[g]
 
 
 def decompose(domain: Box, max_grid_size) -> BoxArray:
-    """Chop a domain into boxes of extent <= max_grid_size, x fastest."""
-    m = [max_grid_size] * len(domain.lo) if isinstance(max_grid_size, int) else list(max_grid_size)
-    per_axis = []
-    for lo, hi, s in zip(domain.lo, domain.hi, m):
-        starts = list(range(lo, hi + 1, s))
-        per_axis.append([(a, min(a + s - 1, hi)) for a in starts])
-    boxes = []
-    for combo in itertools.product(*per_axis[::-1]):
+    """Cut ``domain`` into boxes no longer than max_grid_size per axis;
+    box k = ix + nbx*(iy + nby*iz) (x fastest), like core/mesh.py:223-235."""
+    dim = len(domain.lo)
+    sizes = [max_grid_size] * dim if isinstance(max_grid_size, int) else [int(v) for v in max_grid_size]
+    spans = []
+    for d in range(dim):
+        cuts = range(domain.lo[d], domain.hi[d] + 1, sizes[d])
+        spans.append([(c, min(c + sizes[d], domain.hi[d] + 1) - 1) for c in cuts])
+    out = []
+    for combo in itertools.product(*spans[::-1]):
         combo = combo[::-1]
-        boxes.append(Box([c[0] for c in combo], [c[1] for c in combo], domain.ixtype))
-    return BoxArray(boxes)
+        out.append(Box(tuple(c[0] for c in combo), tuple(c[1] for c in combo), domain.ixtype))
+    return BoxArray(out)
 
 
 class DistributionMapping:
-    """Owning rank per BoxArray entry."""
+    """Owner rank of every BoxArray entry."""
 
     def __init__(self, rank_of: Iterable[int], nranks: int | None = None):
-        self.rank_of = tuple(int(r) for r in rank_of)
-        self.nranks = int(nranks) if nranks is not None else (max(self.rank_of) + 1 if self.rank_of else 1)
-        if any(r < 0 or r >= self.nranks for r in self.rank_of):
-            raise ValueError("rank ids must lie in [0, nranks)")
+        owners = tuple(int(r) for r in rank_of)
+        self.rank_of = owners
+        self.nranks = int(nranks) if nranks is not None else (1 + max(owners) if owners else 1)
+        if owners and (min(owners) < 0 or max(owners) >= self.nranks):
+            raise ValueError(f"DistributionMapping: ranks must be in [0, {self.nranks})")
         self.uid = _next_uid()
-        self._arr = np.ascontiguousarray(np.asarray(self.rank_of, dtype=np.int32))
+        self._arr = np.ascontiguousarray(np.asarray(owners, dtype=np.int32))
 
     @staticmethod
     def round_robin(nboxes: int, nranks: int) -> "DistributionMapping":
-        return DistributionMapping([i % nranks for i in range(nboxes)], nranks)
+        return DistributionMapping([k % nranks for k in range(nboxes)], nranks)
 
     def __len__(self) -> int:
         return len(self.rank_of)

@@ -345,6 +345,11 @@ def run_ours(args, cfg, rank, world):
     torch.cuda.synchronize()
     # device-timed region
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    # write_read: after the 512 MiB write, read a clean 256 MiB buffer so the
+    # flush's dirty lines are written back before the timed region instead of
+    # inside it (the kernel then starts from a cold, clean L2, like ncu's
+    # --cache-control all)
+    clean = torch.ones(64 << 20, dtype=torch.int32, device=dev) if args.l2 == "write_read" else None
     K = args.steps
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
@@ -356,6 +361,8 @@ def run_ours(args, cfg, rank, world):
     with ClockSampler(dev) as clk:
         for i in range(K):
             flush.zero_()
+            if clean is not None:
+                torch.sum(clean)
             ev0[i].record(stream)
             if can_enqueue:
                 x.enqueue(stream.cuda_stream)
@@ -433,7 +440,10 @@ def run_ours(args, cfg, rank, world):
                    "transport": x.transport if world > 1 else "local",
                    "sync": x.sync if world > 1 else None,
                    "remote": x.remote if world > 1 else None,
-                   "l2": "flushed before every step (512 MiB write, outside the events)",
+                   "l2": ("flushed before every step (512 MiB write, then a 256 MiB clean read so no dirty "
+                          "flush lines are written back inside the timed region; outside the events)"
+                          if args.l2 == "write_read" else
+                          "flushed before every step (512 MiB write, outside the events)"),
                    "tags_this_rank": x.ex.ntags if x.transport == "p2p" else None,
                    "warp_tasks_this_rank": x.ex.ntasks if x.transport == "p2p" else None,
                    "exec": x.ex.detail if x.transport == "p2p" else None},
@@ -510,6 +520,8 @@ def main():
                     help="default C2 = BASELINE.json configs[1] (the 1-B200 config), weak-scaled for N>1")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--transport", default=None, choices=["p2p", "nccl"])
+    ap.add_argument("--l2", default="write_read", choices=["write", "write_read"],
+                    help="L2 flush between timed steps (both outside the events)")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-e2e", action="store_true")

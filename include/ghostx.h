@@ -174,6 +174,47 @@ int ghx_fill_hash_wrapped(void *fab, const int64_t fab_box[6], int32_t ncomp, co
 /* Number of fused-copy kernel launches issued by this process. */
 int64_t ghx_launch_count(void);
 
+/* ------------------------------------------------ coarse/fine transfers */
+
+#define GHX_INTERP_PC 0     /* amr.PIECEWISE_CONSTANT */
+#define GHX_INTERP_LINEAR 1 /* amr.LINEAR: unlimited centred slopes */
+
+/* One interp_box job (reference amr.py:269-314): fill `region` (fine
+ * index space) of the fine fab from the coarse fab.  Boxes are the fabs'
+ * storage boxes, padded to 3 axes (lo = hi = 0).  Requires region inside
+ * fine_box and coarsen(region) (grown by 1 on axes < spacedim for LINEAR)
+ * inside crse_box, else GHX_EINVAL ("insufficient coarse data"). */
+typedef struct {
+  const void *crse;
+  int64_t crse_box[6];
+  void *fine;
+  int64_t fine_box[6];
+  int64_t region[6];
+} ghx_interp_job;
+
+/* Every job in ONE launch on `stream`; ncomp components (both fabs), ratio
+ * per axis (1 on axes >= spacedim), float64 or float32 storage.  Results
+ * are bit-identical to numpy's evaluation order in interp_box. */
+int ghx_interp(const ghx_interp_job *jobs, int64_t njobs, int32_t ncomp, const int32_t ratio[3], int32_t spacedim,
+               int32_t scheme, int32_t elem_bytes, void *stream);
+
+/* One restriction job of average_down (amr.py:251-264): every coarse cell
+ * of `region` (coarse index space) becomes the mean of its ratio^D fine
+ * children (summed in (oz, oy, ox) order, divided by ratio^spacedim). */
+typedef struct {
+  const void *fine;
+  int64_t fine_box[6];
+  void *crse;
+  int64_t crse_box[6];
+  int64_t region[6];
+} ghx_avgdown_job;
+
+int ghx_average_down(const ghx_avgdown_job *jobs, int64_t njobs, int32_t ncomp, const int32_t ratio[3],
+                     int32_t spacedim, int32_t elem_bytes, void *stream);
+
+/* Number of interp / average_down launches issued by this process. */
+int64_t ghx_amr_launch_count(void);
+
 #ifdef __cplusplus
 }
 #endif

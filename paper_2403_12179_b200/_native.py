@@ -65,7 +65,14 @@ _SIGS = {
     "ghx_fill_hash": (C.c_int, [P, PI64, I32, PI64, PI64, C.c_uint64, I32, P]),
     "ghx_fill_hash_wrapped": (C.c_int, [P, PI64, I32, PI64, PI32, C.c_uint64, I32, P]),
     "ghx_launch_count": (I64, []),
+    # job arrays: int64[njobs, 20] rows laid out like ghx_interp_job / ghx_avgdown_job
+    "ghx_interp": (C.c_int, [P, I64, I32, PI32, I32, I32, I32, P]),
+    "ghx_average_down": (C.c_int, [P, I64, I32, PI32, I32, I32, P]),
+    "ghx_amr_launch_count": (I64, []),
 }
+
+INTERP_PC, INTERP_LINEAR = 0, 1
+JOB_WORDS = 20  # int64 words per ghx_interp_job / ghx_avgdown_job
 
 EXPORTED = tuple(_SIGS)
 

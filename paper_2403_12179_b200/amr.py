@@ -1,0 +1,233 @@
+"""Coarse/fine level transfers on top of the exchange engine: fill_patch
+(FillBoundary + gather of coarse data + interpolation), average_down
+(restriction + ParallelCopy) and interp_box.
+
+Drop-in for the reference's level-transfer functions
+(/root/reference/pkg/src/miniamr_core/amr.py:235-397): same names, argument
+meaning, validation order and ValueErrors.  The exchange steps run on the
+fused copy kernel (ghx_exec.cu), the local arithmetic on ghx_amr.cu, one
+launch per call for all fabs (the reference's ``fused_segments``).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _native as N
+from . import comm, config
+from .index_space import Box, Geometry, IntVect, box_diff, box_list_diff, coarsen, grow, intersect
+from .mesh import BoxArray, Fab, MultiFab
+
+PIECEWISE_CONSTANT = "piecewise_constant"
+LINEAR = "linear"
+_SCHEMES = {PIECEWISE_CONSTANT: N.INTERP_PC, LINEAR: N.INTERP_LINEAR}
+
+
+def _pad(vals, fill: int) -> list:
+    v = list(vals)
+    return v + [fill] * (3 - len(v))
+
+
+def _row(b: Box) -> list:
+    return list(b.as_row())
+
+
+def _ratio3(ratio: int) -> np.ndarray:
+    return np.asarray(_pad([ratio] * config.spacedim, 1), np.int32)
+
+
+def _stream(device: int) -> int:
+    import torch
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _sync(device: int) -> None:
+    import torch
+    torch.cuda.current_stream(device).synchronize()
+
+
+def _launch_interp(jobs: list, ncomp: int, ratio: int, scheme: str, item: int, device: int) -> None:
+    """jobs: (coarse Fab, fine Fab, fine region) -> one ghx_interp launch."""
+    if not jobs:
+        return
+    rows = np.zeros((len(jobs), N.JOB_WORDS), np.int64)
+    for n, (cf, ff, region) in enumerate(jobs):
+        rows[n, 0] = np.uint64(cf.ptr).view(np.int64)
+        rows[n, 1:7] = _row(cf.box)
+        rows[n, 7] = np.uint64(ff.ptr).view(np.int64)
+        rows[n, 8:14] = _row(ff.box)
+        rows[n, 14:20] = _row(region)
+    r3 = _ratio3(ratio)
+    N.check(N.lib.ghx_interp(C.c_void_p(rows.ctypes.data), len(jobs), ncomp, N.i32p(r3), config.spacedim,
+                             _SCHEMES[scheme], item, C.c_void_p(_stream(device))))
+
+
+def interp_box(coarse_fab: Fab, fine_fab: Fab, fine_region: Box, ratio: int,
+               scheme: str = PIECEWISE_CONSTANT) -> None:
+    """Fill fine_region of fine_fab from coarse_fab data (amr.py:269-314).
+
+    LINEAR uses unlimited centred slopes, so globally linear coarse data is
+    reproduced exactly at fine cell centres; it needs one extra coarse cell
+    around the coarsened region, else this raises."""
+    if fine_region.is_empty:
+        return
+    ratio = int(ratio)
+    if not fine_fab.box.contains(fine_region):
+        raise ValueError("fine_region must lie inside the fine fab")
+    creg = coarsen(fine_region, ratio)
+    need = grow(creg, 1) if scheme == LINEAR else creg
+    if not coarse_fab.box.contains(need):
+        raise ValueError(f"insufficient coarse data: need {need} inside {coarse_fab.box}")
+    if scheme not in (PIECEWISE_CONSTANT, LINEAR):
+        raise ValueError(f"unknown interpolation scheme {scheme!r}")
+    if coarse_fab.ncomp != fine_fab.ncomp:
+        raise ValueError(f"component count mismatch: coarse {coarse_fab.ncomp}, fine {fine_fab.ncomp}")
+    if coarse_fab.dtype != fine_fab.dtype or coarse_fab.device != fine_fab.device:
+        raise ValueError("coarse and fine fabs must share the real type and the device")
+    _launch_interp([(coarse_fab, fine_fab, fine_region)], fine_fab.ncomp, ratio, scheme,
+                   fine_fab.dtype.itemsize, fine_fab.device)
+    _sync(fine_fab.device)
+
+
+def interp_coarse_to_fine(coarse_fab: Fab, fine_fab: Fab, fine_region: Box, ratio: int,
+                          scheme: str = PIECEWISE_CONSTANT) -> None:
+    interp_box(coarse_fab, fine_fab, fine_region, ratio, scheme)
+
+
+# -------------------------------------------------------------- average_down
+
+def _restriction_layout(fine: MultiFab, ratio: int) -> MultiFab:
+    """tmp MultiFab over coarsen(fine.ba) with fine's DistributionMapping
+    (amr.py:247-249), cached on fine so the ParallelCopy plan into a given
+    coarse MultiFab is built once (the reference rebuilds both per call)."""
+    key = ("average_down_tmp", fine.ba.uid, fine.dm.uid, ratio, fine.ncomp, fine.dtype.str)
+    tmp = fine._peer_cache.get(key)
+    if tmp is None:
+        crse_ba = BoxArray([coarsen(b, ratio) for b in fine.ba])
+        tmp = fine._peer_cache[key] = MultiFab(crse_ba, fine.dm, fine.ncomp, 0, rank=fine.rank, device=fine.device)
+    return tmp
+
+
+def average_down(fine: MultiFab, coarse: MultiFab, ratio: int, backend=None) -> None:
+    """Covered coarse cells become the mean of their ratio^D fine children
+    (amr.py:235-266): one restriction launch over the local fine fabs, then
+    ParallelCopy into ``coarse``."""
+    ratio = int(ratio)
+    if ratio < 1:
+        raise ValueError("ratio must be >= 1")
+    for b in fine.ba:
+        if any(e % ratio for e in b.extents) or any(lo % ratio for lo in b.lo):
+            raise ValueError(f"fine box {b} is not aligned to ratio {ratio}")
+    if fine.ncomp != coarse.ncomp:
+        raise ValueError("component count mismatch")
+    tmp = _restriction_layout(fine, ratio)
+    rows = np.zeros((len(fine.local_indices), N.JOB_WORDS), np.int64)
+    for n, gi in enumerate(fine.local_indices):
+        ff, tf = fine.fabs[gi], tmp.fabs[gi]
+        rows[n, 0] = np.uint64(ff.ptr).view(np.int64)
+        rows[n, 1:7] = _row(ff.box)
+        rows[n, 7] = np.uint64(tf.ptr).view(np.int64)
+        rows[n, 8:14] = _row(tf.box)
+        rows[n, 14:20] = _row(tmp.ba[gi])
+    if len(rows):
+        N.check(N.lib.ghx_average_down(C.c_void_p(rows.ctypes.data), len(rows), fine.ncomp,
+                                       N.i32p(_ratio3(ratio)), config.spacedim, fine.dtype.itemsize,
+                                       C.c_void_p(_stream(fine.device))))
+    comm.parallel_copy(coarse, tmp, backend=backend)
+
+
+# ---------------------------------------------------------------- fill_patch
+
+def _same_level_sources(ba: BoxArray, geom: Geometry) -> list:
+    """Valid boxes plus their periodic images (amr.py:322-331)."""
+    out = []
+    reach = IntVect.filled(max(g for g in geom.period))
+    big = grow(geom.domain, reach)
+    for b in ba:
+        out.append(b)
+        for s in _shift_candidates(b, big, geom):
+            if any(v != 0 for v in s):
+                out.append(b.shift(s))
+    return out
+
+
+def _shift_candidates(src_box: Box, target: Box, geom: Geometry | None) -> list:
+    """Period multiples moving src_box onto target (comm.py:250-266)."""
+    import itertools
+    import math
+    dim = len(src_box.lo)
+    if geom is None:
+        return [IntVect.zero()]
+    per_axis = []
+    for d in range(dim):
+        if not geom.periodic[d]:
+            per_axis.append([0])
+            continue
+        ext = geom.period[d]
+        kmin = math.ceil((target.lo[d] - src_box.hi[d]) / ext)
+        kmax = math.floor((target.hi[d] - src_box.lo[d]) / ext)
+        if kmin > kmax:
+            return []
+        per_axis.append([k * ext for k in range(kmin, kmax + 1)])
+    return [IntVect(*c) for c in itertools.product(*per_axis)]
+
+
+def _coarse_fill_targets(fine_ba: BoxArray, ngrow: IntVect, geom: Geometry) -> dict:
+    """Per fine fab: ghost boxes not coverable by same-level valid data
+    (amr.py:334-352); non-periodic axes clip at the domain."""
+    sources = _same_level_sources(fine_ba, geom)
+    clip_lo, clip_hi = [], []
+    big = max(geom.period) + max(ngrow) + 1
+    for d in range(config.spacedim):
+        clip_lo.append(geom.domain.lo[d] - (big if geom.periodic[d] else 0))
+        clip_hi.append(geom.domain.hi[d] + (big if geom.periodic[d] else 0))
+    clip = Box(clip_lo, clip_hi)
+    out = {}
+    for gi, b in enumerate(fine_ba):
+        ghost = box_diff(grow(b, ngrow), b)
+        rest = box_list_diff(ghost, sources)
+        rest = [intersect(r, clip) for r in rest]
+        rest = [r for r in rest if not r.is_empty]
+        if rest:
+            out[gi] = rest
+    return out
+
+
+def fill_patch(fine: MultiFab, coarse: MultiFab, fine_geom: Geometry, coarse_geom: Geometry, ratio: int,
+               scheme: str = LINEAR, backend=None) -> None:
+    """Fill fine ghost cells: same-level data where available, interpolated
+    coarse data elsewhere; valid cells are never modified (amr.py:355-397).
+
+    FillBoundary (fused exchange) -> gather of the coarse cells under each
+    fine fab's uncovered ghost regions (fused exchange, plan-cached target
+    slab) -> one interp launch over every (fab, region) job."""
+    comm.fill_boundary(fine, fine_geom, backend=backend)
+    reach = 1 if scheme == LINEAR else 0
+    key = comm.PlanKey(coarse.ba.uid, coarse.dm.uid, fine.ba.uid, fine.dm.uid, (reach,) * len(fine.ngrow),
+                       fine.ngrow.comps, fine.ba.ixtype.flags, fine_geom.periodic, "fill_patch")
+    cached = fine.plan_cache.get(key)
+    if cached is None:
+        targets = _coarse_fill_targets(fine.ba, fine.ngrow, fine_geom)
+        gather_list, dst_ranks = [], []
+        for gi in sorted(targets):
+            cbox = grow(coarsen(grow(fine.ba[gi], fine.ngrow), ratio), reach)
+            gather_list.append((gi, cbox))
+            dst_ranks.append(fine.dm[gi])
+        plan = comm.build_gather_plan(gather_list, dst_ranks, coarse, coarse_geom) if gather_list else None
+        cached = (targets, gather_list, dst_ranks, plan)
+        fine.plan_cache[key] = cached
+        fine.plan_builds += 1
+    targets, gather_list, dst_ranks, plan = cached
+    if not targets:
+        return
+    owned = comm.gather_targets(plan, gather_list, dst_ranks, coarse)
+    comm.gather_fabs(gather_list, dst_ranks, owned, coarse, coarse_geom, backend=backend, plan=plan)
+    jobs = [(owned[gi], fine.fabs[gi], region) for gi in sorted(targets) if gi in owned
+            for region in targets[gi]]
+    for cf, ff, region in jobs:  # interp_box's checks, before the one launch
+        if not ff.box.contains(region):
+            raise ValueError("fine_region must lie inside the fine fab")
+    _launch_interp(jobs, fine.ncomp, int(ratio), scheme, fine.dtype.itemsize, fine.device)
+    _sync(fine.device)

@@ -959,3 +959,115 @@ def parallel_copy(dst: MultiFab, src: MultiFab, scomp: int = 0, dcomp: int = 0, 
     ctx = current_ctx()
     _execute_plan(plan, src, dst, scomp, dcomp, ncomp, ctx, backend)
     ctx.barrier()
+
+
+# ------------------------------------------------------------------ gathers
+
+class _FabSet:
+    """The private destination fabs of a gather (comm.py:432-462), laid out
+    like a MultiFab for the exchange engine: position p of the global
+    dst_fabs list is dst slot p; this rank's positions live in one slab (so
+    process-mode peers can map it with CUDA IPC)."""
+
+    def __init__(self, boxes: list, ranks: list, ncomp: int, dtype, device: int, rank: int, dim: int):
+        from .mesh import _ALIGN, Slab, Fab, _next_uid
+        self.ncomp = int(ncomp)
+        self.dtype = dtype
+        self.device = int(device)
+        self.ngrow = IntVect(*([0] * dim))
+        self.uid = _next_uid()
+        self._peer_cache: dict = {}
+        self._rows = np.ascontiguousarray(np.asarray([b.as_row() for b in boxes], np.int64).reshape(-1, 6))
+        self.local_indices = tuple(p for p, r in enumerate(ranks) if r == rank)
+        item = np.dtype(dtype).itemsize
+        offs, total = {}, 0
+        for p in self.local_indices:
+            offs[p] = total // item
+            total += -(-boxes[p].num_pts * self.ncomp * item // _ALIGN) * _ALIGN
+        self._slab = Slab(max(total, 256), self.device) if self.local_indices else None
+        if self._slab is not None and config.debug:  # fresh fabs are poisoned, like Fab()
+            N.check(N.lib.ghx_memset_u64(C.c_void_p(self._slab.ptr), config.POISON_BITS64 if item == 8
+                                         else (config.POISON_BITS32 << 32) | config.POISON_BITS32,
+                                         -(-total // 8), None))
+        self.fabs = {p: Fab(boxes[p], self.ncomp, _slab=self._slab, _offset=offs[p]) for p in self.local_indices}
+        self._ptrs = np.array([self.fabs[p].ptr for p in self.local_indices], np.uint64)
+
+    def storage_rows(self) -> np.ndarray:
+        return self._rows
+
+
+def build_gather_plan(dst_fabs: list, dst_ranks: list, src: MultiFab, geom: Geometry | None = None) -> CommPlan:
+    """Plan a collective gather of src valid data into private target fabs
+    (reference comm.py:432-443): every (fab_id, box) of ``dst_fabs`` (the
+    same list on every rank; boxes may overlap) receives the overlapping
+    valid cells of src, periodic images included when ``geom`` is given."""
+    boxes = [b for _, b in dst_fabs]
+    nranks = max(src.dm.nranks, max(dst_ranks, default=0) + 1)
+    if not boxes:
+        h = C.c_void_p()
+        rows = np.zeros((0, 6), np.int64)
+        N.check(N.lib.ghx_plan_build_parallel_copy(0, N.i64p(rows), N.i64p(np.zeros(3, np.int64)), len(src.ba),
+                                                   N.i64p(src.ba.rows()), N.i64p(np.zeros(3, np.int64)), None, None,
+                                                   N.i32p(src.dm.array()), N.i32p(np.zeros(0, np.int32)), nranks,
+                                                   C.byref(h)))
+        return CommPlan(h.value, nranks, len(src.ngrow), src.ba.ixtype)
+    rows = np.ascontiguousarray(np.asarray([b.as_row() for b in boxes], np.int64))
+    per = period = None
+    if geom is not None:
+        per = np.zeros(3, np.int32)
+        per[:len(geom.periodic)] = geom.periodic
+        period = np.ones(3, np.int64)
+        period[:len(geom.period)] = geom.period
+    zero = np.zeros(3, np.int64)
+    h = C.c_void_p()
+    N.check(N.lib.ghx_plan_build_parallel_copy(
+        len(boxes), N.i64p(rows), N.i64p(zero), len(src.ba), N.i64p(src.ba.rows()), N.i64p(zero.copy()),
+        N.i32p(per) if per is not None else None, N.i64p(period) if period is not None else None,
+        N.i32p(src.dm.array()), N.i32p(np.asarray(dst_ranks, np.int32)), nranks, C.byref(h)))
+    return CommPlan(h.value, nranks, len(src.ngrow), src.ba.ixtype)
+
+
+def _gather_set(plan: CommPlan, dst_fabs: list, dst_ranks: list, src: MultiFab) -> _FabSet:
+    ctx = current_ctx()
+    key = ("gather_set", src.uid, ctx.rank, src.ncomp)
+    fs = plan._execs.get(key)
+    if fs is None:
+        fs = plan._execs[key] = _FabSet([b for _, b in dst_fabs], list(dst_ranks), src.ncomp, src.dtype,
+                                        src.device, ctx.rank, len(src.ngrow))
+    return fs
+
+
+def gather_fabs(dst_fabs: list, dst_ranks: list, owned: dict, src: MultiFab, geom: Geometry | None = None,
+                backend=None, plan: CommPlan | None = None) -> None:
+    """Collective gather of src valid data into caller-private fabs
+    (reference comm.py:446-462).  ``owned`` maps this rank's fab ids to
+    destination Fabs over exactly their dst_fabs boxes.  The exchange lands
+    in a plan-cached device slab (one fused launch, peers write it directly
+    in process mode), then each owned Fab receives its target region with
+    one device copy; pass the plan's own fabs (``gather_targets``) to skip
+    that copy."""
+    if plan is None:
+        plan = build_gather_plan(dst_fabs, dst_ranks, src, geom)
+    if plan.is_empty:
+        return
+    fs = _gather_set(plan, dst_fabs, dst_ranks, src)
+    ctx = current_ctx()
+    _execute_plan(plan, src, fs, 0, 0, src.ncomp, ctx, backend)
+    pos_of = {fid: pos for pos, (fid, _) in enumerate(dst_fabs)}
+    for fid, fab in owned.items():
+        mine = fs.fabs.get(pos_of[fid])
+        if mine is None:
+            raise ValueError(f"gather_fabs: fab {fid} is not a target of rank {ctx.rank}")
+        if fab.data is not mine.data:
+            if fab.box != mine.box or fab.ncomp != mine.ncomp:
+                raise ValueError(f"gather_fabs: owned fab {fid} does not match its target box {mine.box}")
+            fab.data.copy_(mine.data)
+    ctx.barrier()
+
+
+def gather_targets(plan: CommPlan, dst_fabs: list, dst_ranks: list, src: MultiFab) -> dict:
+    """This rank's plan-cached gather destination fabs, by fab id (fill_patch
+    gathers straight into them)."""
+    fs = _gather_set(plan, dst_fabs, dst_ranks, src)
+    return {fid: fs.fabs[pos] for pos, (fid, _) in enumerate(dst_fabs) if pos in fs.fabs}
+

@@ -1,0 +1,189 @@
+"""Coarse/fine level-transfer throughput on one B200 (SURVEY.md section 8f
+rows 1-2): fill_patch (FillBoundary + coarse gather + interpolation) and
+average_down (restriction + ParallelCopy).
+
+    python bench_amr.py [--op fill_patch|average_down] [--steps K] [--warmup W]
+
+Workload (synthetic, splitmix64 hash data): a 256^3 periodic coarse level
+cut into 64^3 boxes, ncomp 4, float64; the fine level refines the central
+128^3 coarse cells by 2 (a 256^3 fine patch of 64 boxes of 64^3, nghost 2).
+fill_patch is LINEAR.  One JSON line per op: whole-call time (CUDA events
+around the public call, L2 flushed before each step), the dominant kernel's
+event time against the measured HBM copy bandwidth, and the numpy oracle of
+the reference arithmetic timed on a sample on the host.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import sys
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+N_CRSE, BOX, NCOMP, NGROW, RATIO = 256, 64, 4, 2, 2
+PATCH_LO, PATCH_HI = 64, 191  # coarse cells refined
+
+
+def peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def layout(amr):
+    amr.config.set_spacedim(3)
+    cdom = amr.Box((0, 0, 0), (N_CRSE - 1,) * 3)
+    cgeom = amr.Geometry(cdom, (0.0,) * 3, (1.0,) * 3, (True,) * 3)
+    fgeom = cgeom.refined(RATIO)
+    cba = amr.decompose(cdom, BOX)
+    patch = amr.Box((PATCH_LO * RATIO,) * 3, ((PATCH_HI + 1) * RATIO - 1,) * 3)
+    fba = amr.decompose(patch, BOX)
+    return cdom, cgeom, fgeom, cba, fba
+
+
+def timed(fn, steps, warmup, flush, clean):
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(steps):
+        flush.zero_()
+        torch.sum(clean)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1e-3)
+    return statistics.mean(ts), min(ts)
+
+
+def run(args):
+    import torch
+    import paper_2403_12179_b200 as amr
+    from paper_2403_12179_b200 import _native as N
+    from paper_2403_12179_b200 import amr as A
+    torch.cuda.set_device(0)
+    cdom, cgeom, fgeom, cba, fba = layout(amr)
+    coarse = amr.MultiFab(cba, amr.DistributionMapping([0] * len(cba)), NCOMP, 0, cgeom)
+    fine = amr.MultiFab(fba, amr.DistributionMapping([0] * len(fba)), NCOMP, NGROW, fgeom)
+    coarse.fill_hash(20261018, cdom)
+    fine.fill_hash(20261017, fgeom.domain)
+    torch.cuda.synchronize()
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    clean = torch.ones(64 << 20, dtype=torch.int32, device="cuda")
+    hbm, peak_src = peaks()
+    item = 8
+    out = {"op": args.op, "unit": "GB/s", "dtype": "f64", "steps": args.steps, "warmup": args.warmup,
+           "data": "synthetic (splitmix64 hash valid cells)",
+           "config": {"workload": f"coarse {N_CRSE}^3 periodic / {BOX}^3 boxes, fine patch = coarse cells "
+                                  f"[{PATCH_LO},{PATCH_HI}]^3 refined x{RATIO} ({len(fba)} boxes of {BOX}^3, "
+                                  f"nghost {NGROW}), ncomp {NCOMP}, float64",
+                      "l2": "flushed before every step (512 MiB write + 256 MiB clean read, outside the events)"}}
+    if args.op == "fill_patch":
+        call = lambda: A.fill_patch(fine, coarse, fgeom, cgeom, RATIO, A.LINEAR)  # noqa: E731
+        t_mean, t_min = timed(call, args.steps, args.warmup, flush, clean)
+        ghost_cells = sum(amr.grow(b, NGROW).num_pts - b.num_pts for b in fba)
+        ghost_bytes = ghost_cells * NCOMP * item
+        # the interp launch alone: the plan-cached prepared transfer
+        key = [k for k in fine.plan_cache if getattr(k, "op", "") == "fill_patch"][0]
+        targets = fine.plan_cache[key][0]
+        xf = [v for k, v in fine._peer_cache.items() if isinstance(k, tuple) and k[0] == "fill_patch_interp"][0]
+        regions = [r for gi in targets for r in targets[gi]]
+        interp_cells = sum(r.num_pts for r in regions)
+        assert interp_cells == xf.cells
+        # coarse cells the LINEAR stencil reads (parents grown by 1), per region
+        crse_cells = sum(amr.grow(amr.coarsen(r, RATIO), 1).num_pts for r in regions)
+        k_mean, _ = timed(xf.run, args.steps, args.warmup, flush, clean)
+        alg = (interp_cells + crse_cells) * NCOMP * item
+        out.update(metric="fill_patch fine-ghost GB/s (FillBoundary + coarse gather + LINEAR interp)",
+                   value=round(ghost_bytes / t_mean / 1e9, 2), ms_per_step=round(t_mean * 1e3, 4),
+                   ghost_bytes_per_step=ghost_bytes, interp_cells=interp_cells,
+                   roofline={"kernel": "interp_kernel<double,LINEAR>", "bound": "hbm",
+                             "algorithmic_bytes_per_launch": alg,
+                             "achieved": round(alg / k_mean / 1e9, 1), "peak": hbm,
+                             "frac": round(alg / k_mean / 1e9 / hbm, 4), "unit": "GB/s", "peak_source": peak_src,
+                             "kernel_ms": round(k_mean * 1e3, 4)})
+        out["cpu_baseline"] = cpu_interp_sample(fine, targets)
+    else:
+        crse_fine = amr.MultiFab(cba, amr.DistributionMapping([0] * len(cba)), NCOMP, 0, cgeom)
+        call = lambda: A.average_down(fine, crse_fine, RATIO)  # noqa: E731
+        t_mean, t_min = timed(call, args.steps, args.warmup, flush, clean)
+        fine_cells = sum(b.num_pts for b in fba)
+        crse_cells = fine_cells // RATIO ** 3
+        xf = [v for k, v in fine._peer_cache.items() if isinstance(k, tuple) and k[0] == "average_down_xfer"][0]
+        k_mean, _ = timed(xf.run, args.steps, args.warmup, flush, clean)
+        alg = (fine_cells + crse_cells) * NCOMP * item
+        out.update(metric="average_down GB/s (fine bytes restricted, restriction + ParallelCopy)",
+                   value=round(fine_cells * NCOMP * item / t_mean / 1e9, 2), ms_per_step=round(t_mean * 1e3, 4),
+                   roofline={"kernel": "avgdown_kernel<double>", "bound": "hbm", "algorithmic_bytes_per_launch": alg,
+                             "achieved": round(alg / k_mean / 1e9, 1), "peak": hbm,
+                             "frac": round(alg / k_mean / 1e9 / hbm, 4), "unit": "GB/s", "peak_source": peak_src,
+                             "kernel_ms": round(k_mean * 1e3, 4)})
+        out["cpu_baseline"] = cpu_restrict_sample()
+    out["amr_launches"] = int(N.lib.ghx_amr_launch_count())
+    print(json.dumps(out), flush=True)
+
+
+def cpu_interp_sample(fine_mf, targets, seconds=5.0):
+    """numpy oracle of interp_box (reference arithmetic) on the first regions."""
+    import paper_2403_12179_b200 as amr
+    from oracle import amr_oracle as ao
+    rng = np.random.default_rng(1)
+    t0 = time.perf_counter()
+    done = 0
+    jobs = [(gi, r) for gi in sorted(targets) for r in targets[gi]]
+    for gi, region in jobs[:64]:
+        fb = amr.grow(fine_mf.ba[gi], NGROW)
+        cb = amr.grow(amr.coarsen(fb, RATIO), 1)
+        crse = rng.random(tuple(cb.extents) + (NCOMP,))
+        fine = np.empty(tuple(fb.extents) + (NCOMP,))
+        ao.interp(crse, np.asarray(cb.as_row()), fine, np.asarray(fb.as_row()), np.asarray(region.as_row()),
+                  [RATIO] * 3, True, 3)
+        done += region.num_pts
+        if time.perf_counter() - t0 > seconds:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": round(done * NCOMP * 8 / dt / 1e9, 3), "unit": "GB/s (interpolated fine bytes)", "cores": 1,
+            "kind": "port", "sample": f"oracle interp (reference amr.py:269-314 arithmetic) on {done} fine cells"}
+
+
+def cpu_restrict_sample(seconds=5.0):
+    from oracle import amr_oracle as ao
+    rng = np.random.default_rng(2)
+    fine = rng.random((BOX + 2 * NGROW,) * 3 + (NCOMP,))
+    fb = np.asarray([-NGROW] * 3 + [BOX + NGROW - 1] * 3)
+    vb = np.asarray([0] * 3 + [BOX - 1] * 3)
+    t0 = time.perf_counter()
+    n = 0
+    while time.perf_counter() - t0 < seconds and n < 50:
+        ao.restrict(fine, fb, vb, [RATIO] * 3, 3)
+        n += 1
+    dt = time.perf_counter() - t0
+    return {"value": round(n * BOX ** 3 * NCOMP * 8 / dt / 1e9, 3), "unit": "GB/s (fine bytes restricted)",
+            "cores": 1, "kind": "port", "sample": f"oracle restriction (amr.py:251-264) of one {BOX}^3 fab x{n}"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--op", default="fill_patch", choices=["fill_patch", "average_down"])
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    run(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -212,6 +212,19 @@ typedef struct {
 int ghx_average_down(const ghx_avgdown_job *jobs, int64_t njobs, int32_t ncomp, const int32_t ratio[3],
                      int32_t spacedim, int32_t elem_bytes, void *stream);
 
+/* Prepared transfers: the job table is validated and uploaded once
+ * (device `device`), each ghx_xfer_run is one launch on `stream` with no
+ * host-side work (fill_patch / average_down cache one per plan).  Fab
+ * pointers are baked in: the fabs must outlive the handle. */
+typedef struct ghx_xfer ghx_xfer;
+int ghx_interp_prepare(const ghx_interp_job *jobs, int64_t njobs, int32_t ncomp, const int32_t ratio[3],
+                       int32_t spacedim, int32_t scheme, int32_t elem_bytes, int32_t device, ghx_xfer **out);
+int ghx_average_down_prepare(const ghx_avgdown_job *jobs, int64_t njobs, int32_t ncomp, const int32_t ratio[3],
+                             int32_t spacedim, int32_t elem_bytes, int32_t device, ghx_xfer **out);
+int ghx_xfer_run(ghx_xfer *x, void *stream);
+int64_t ghx_xfer_cells(const ghx_xfer *x); /* cells written per run */
+void ghx_xfer_free(ghx_xfer *x);
+
 /* Number of interp / average_down launches issued by this process. */
 int64_t ghx_amr_launch_count(void);
 

@@ -69,6 +69,11 @@ _SIGS = {
     "ghx_interp": (C.c_int, [P, I64, I32, PI32, I32, I32, I32, P]),
     "ghx_average_down": (C.c_int, [P, I64, I32, PI32, I32, I32, P]),
     "ghx_amr_launch_count": (I64, []),
+    "ghx_interp_prepare": (C.c_int, [P, I64, I32, PI32, I32, I32, I32, I32, C.POINTER(P)]),
+    "ghx_average_down_prepare": (C.c_int, [P, I64, I32, PI32, I32, I32, I32, C.POINTER(P)]),
+    "ghx_xfer_run": (C.c_int, [P, P]),
+    "ghx_xfer_cells": (I64, [P]),
+    "ghx_xfer_free": (None, [P]),
 }
 
 INTERP_PC, INTERP_LINEAR = 0, 1

@@ -48,10 +48,28 @@ def _sync(device: int) -> None:
     torch.cuda.current_stream(device).synchronize()
 
 
-def _launch_interp(jobs: list, ncomp: int, ratio: int, scheme: str, item: int, device: int) -> None:
-    """jobs: (coarse Fab, fine Fab, fine region) -> one ghx_interp launch."""
-    if not jobs:
-        return
+class _Xfer:
+    """A prepared interp / average_down launch (ghx_xfer): the job table is
+    validated and uploaded once; ``run`` is one kernel launch."""
+
+    def __init__(self, handle: int, device: int):
+        self._h = C.c_void_p(handle)
+        self.device = device
+        self.cells = int(N.lib.ghx_xfer_cells(self._h))
+
+    def run(self) -> None:
+        N.check(N.lib.ghx_xfer_run(self._h, C.c_void_p(_stream(self.device))))
+
+    def __del__(self):
+        try:
+            if self._h:
+                N.lib.ghx_xfer_free(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
+def _interp_rows(jobs: list) -> np.ndarray:
     rows = np.zeros((len(jobs), N.JOB_WORDS), np.int64)
     for n, (cf, ff, region) in enumerate(jobs):
         rows[n, 0] = np.uint64(cf.ptr).view(np.int64)
@@ -59,9 +77,25 @@ def _launch_interp(jobs: list, ncomp: int, ratio: int, scheme: str, item: int, d
         rows[n, 7] = np.uint64(ff.ptr).view(np.int64)
         rows[n, 8:14] = _row(ff.box)
         rows[n, 14:20] = _row(region)
-    r3 = _ratio3(ratio)
-    N.check(N.lib.ghx_interp(C.c_void_p(rows.ctypes.data), len(jobs), ncomp, N.i32p(r3), config.spacedim,
-                             _SCHEMES[scheme], item, C.c_void_p(_stream(device))))
+    return rows
+
+
+def _prepare_interp(jobs: list, ncomp: int, ratio: int, scheme: str, item: int, device: int) -> _Xfer:
+    """jobs: (coarse Fab, fine Fab, fine region) -> one prepared launch."""
+    rows = _interp_rows(jobs)
+    h = C.c_void_p()
+    N.check(N.lib.ghx_interp_prepare(C.c_void_p(rows.ctypes.data), len(jobs), ncomp, N.i32p(_ratio3(ratio)),
+                                     config.spacedim, _SCHEMES[scheme], item, device, C.byref(h)))
+    return _Xfer(h.value, device)
+
+
+def _launch_interp(jobs: list, ncomp: int, ratio: int, scheme: str, item: int, device: int) -> None:
+    """One-shot: jobs -> one ghx_interp launch."""
+    if not jobs:
+        return
+    rows = _interp_rows(jobs)
+    N.check(N.lib.ghx_interp(C.c_void_p(rows.ctypes.data), len(jobs), ncomp, N.i32p(_ratio3(ratio)),
+                             config.spacedim, _SCHEMES[scheme], item, C.c_void_p(_stream(device))))
 
 
 def interp_box(coarse_fab: Fab, fine_fab: Fab, fine_region: Box, ratio: int,
@@ -123,18 +157,23 @@ def average_down(fine: MultiFab, coarse: MultiFab, ratio: int, backend=None) -> 
     if fine.ncomp != coarse.ncomp:
         raise ValueError("component count mismatch")
     tmp = _restriction_layout(fine, ratio)
-    rows = np.zeros((len(fine.local_indices), N.JOB_WORDS), np.int64)
-    for n, gi in enumerate(fine.local_indices):
-        ff, tf = fine.fabs[gi], tmp.fabs[gi]
-        rows[n, 0] = np.uint64(ff.ptr).view(np.int64)
-        rows[n, 1:7] = _row(ff.box)
-        rows[n, 7] = np.uint64(tf.ptr).view(np.int64)
-        rows[n, 8:14] = _row(tf.box)
-        rows[n, 14:20] = _row(tmp.ba[gi])
-    if len(rows):
-        N.check(N.lib.ghx_average_down(C.c_void_p(rows.ctypes.data), len(rows), fine.ncomp,
-                                       N.i32p(_ratio3(ratio)), config.spacedim, fine.dtype.itemsize,
-                                       C.c_void_p(_stream(fine.device))))
+    key = ("average_down_xfer", fine.ba.uid, fine.dm.uid, ratio, fine.ncomp, fine.dtype.str)
+    xf = fine._peer_cache.get(key)
+    if xf is None:
+        rows = np.zeros((len(fine.local_indices), N.JOB_WORDS), np.int64)
+        for n, gi in enumerate(fine.local_indices):
+            ff, tf = fine.fabs[gi], tmp.fabs[gi]
+            rows[n, 0] = np.uint64(ff.ptr).view(np.int64)
+            rows[n, 1:7] = _row(ff.box)
+            rows[n, 7] = np.uint64(tf.ptr).view(np.int64)
+            rows[n, 8:14] = _row(tf.box)
+            rows[n, 14:20] = _row(tmp.ba[gi])
+        h = C.c_void_p()
+        N.check(N.lib.ghx_average_down_prepare(C.c_void_p(rows.ctypes.data), len(rows), fine.ncomp,
+                                               N.i32p(_ratio3(ratio)), config.spacedim, fine.dtype.itemsize,
+                                               fine.device, C.byref(h)))
+        xf = fine._peer_cache[key] = _Xfer(h.value, fine.device)
+    xf.run()
     comm.parallel_copy(coarse, tmp, backend=backend)
 
 
@@ -224,10 +263,23 @@ def fill_patch(fine: MultiFab, coarse: MultiFab, fine_geom: Geometry, coarse_geo
         return
     owned = comm.gather_targets(plan, gather_list, dst_ranks, coarse)
     comm.gather_fabs(gather_list, dst_ranks, owned, coarse, coarse_geom, backend=backend, plan=plan)
-    jobs = [(owned[gi], fine.fabs[gi], region) for gi in sorted(targets) if gi in owned
-            for region in targets[gi]]
-    for cf, ff, region in jobs:  # interp_box's checks, before the one launch
-        if not ff.box.contains(region):
-            raise ValueError("fine_region must lie inside the fine fab")
-    _launch_interp(jobs, fine.ncomp, int(ratio), scheme, fine.dtype.itemsize, fine.device)
+    xkey = ("fill_patch_interp", key, int(ratio), scheme, fine.ncomp)
+    xf = fine._peer_cache.get(xkey)
+    if xf is None:
+        if coarse.ncomp != fine.ncomp:
+            raise ValueError(f"component count mismatch: coarse {coarse.ncomp}, fine {fine.ncomp}")
+        jobs = [(owned[gi], fine.fabs[gi], region) for gi in sorted(targets) if gi in owned
+                for region in targets[gi]]
+        for cf, ff, region in jobs:  # interp_box's checks (amr.py:281-293), once per plan
+            if not ff.box.contains(region):
+                raise ValueError("fine_region must lie inside the fine fab")
+            creg = coarsen(region, int(ratio))
+            need = grow(creg, 1) if scheme == LINEAR else creg
+            if not cf.box.contains(need):
+                raise ValueError(f"insufficient coarse data: need {need} inside {cf.box}")
+        if scheme not in (PIECEWISE_CONSTANT, LINEAR):
+            raise ValueError(f"unknown interpolation scheme {scheme!r}")
+        xf = fine._peer_cache[xkey] = _prepare_interp(jobs, fine.ncomp, int(ratio), scheme, fine.dtype.itemsize,
+                                                      fine.device)
+    xf.run()
     _sync(fine.device)

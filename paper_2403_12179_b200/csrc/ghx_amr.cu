@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <cstring>
 #include <string>
@@ -49,8 +50,8 @@ struct DevAvgJob {
   int64_t start;
 };
 
-__device__ __forceinline__ int64_t floordiv(int64_t a, int64_t b) {
-  const int64_t q = a / b;
+__device__ __forceinline__ int32_t floordiv32(int32_t a, int32_t b) {
+  const int32_t q = a / b;
   return (q * b > a) ? q - 1 : q;
 }
 
@@ -83,25 +84,27 @@ __device__ __forceinline__ float div_rn(float a, float b) { return __fdiv_rn(a, 
 //   v     = T(double(v) + double(slope) * off)   (numpy's float64 loop for
 //                                                 v += slope * off)
 template <class T, bool LINEAR>
-__global__ void __launch_bounds__(kAmrThreads) interp_kernel(const DevInterpJob *__restrict__ jobs, int njobs,
+__global__ void __launch_bounds__(kAmrThreads, 3) interp_kernel(const DevInterpJob *__restrict__ jobs, int njobs,
                                                              int64_t total, int ncomp, int r0, int r1, int r2,
                                                              int spacedim) {
   const int r[3] = {r0, r1, r2};
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     const DevInterpJob &J = jobs[find_job(jobs, njobs, i)];
-    int64_t q = i - J.start;
-    int64_t fidx[3];
-    fidx[0] = J.rlo[0] + q % J.rn[0];
-    q /= J.rn[0];
-    fidx[1] = J.rlo[1] + q % J.rn[1];
-    fidx[2] = J.rlo[2] + q / J.rn[1];
+    // 32-bit index math inside a job (jobs are < 2^31 cells, host-checked)
+    const uint32_t q = (uint32_t)(i - J.start), nx = (uint32_t)J.rn[0], ny = (uint32_t)J.rn[1];
+    const uint32_t t = q / nx;
+    int32_t fidx[3];
+    fidx[0] = (int32_t)J.rlo[0] + (int32_t)(q - t * nx);
+    fidx[1] = (int32_t)J.rlo[1] + (int32_t)(t % ny);
+    fidx[2] = (int32_t)J.rlo[2] + (int32_t)(t / ny);
     int64_t pl[3];
     double off[3];
+#pragma unroll
     for (int d = 0; d < 3; ++d) {
-      const int64_t p = floordiv(fidx[d], r[d]);
-      pl[d] = p - J.c.lo[d];
-      const int64_t m = fidx[d] - p * r[d];
+      const int32_t p = floordiv32(fidx[d], r[d]);
+      pl[d] = (int64_t)p - J.c.lo[d];
+      const int32_t m = fidx[d] - p * r[d];
       off[d] = __dsub_rn(__ddiv_rn(__dadd_rn((double)m, 0.5), (double)r[d]), 0.5);
     }
     const int64_t csy = J.c.n[0], csz = J.c.n[0] * J.c.n[1], csc = csz * J.c.n[2];
@@ -116,7 +119,9 @@ __global__ void __launch_bounds__(kAmrThreads) interp_kernel(const DevInterpJob 
       const T *cc = crse + co + c * csc;
       T v = __ldg(cc);
       if (LINEAR) {
-        for (int d = 0; d < spacedim; ++d) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          if (d >= spacedim) break;
           const T slope = mul_rn(T(0.5), sub_rn(__ldg(cc + step[d]), __ldg(cc - step[d])));
           v = T(__dadd_rn((double)v, __dmul_rn((double)slope, off[d])));
         }
@@ -129,18 +134,18 @@ __global__ void __launch_bounds__(kAmrThreads) interp_kernel(const DevInterpJob 
 // One thread per coarse cell: acc = child(0,0,0), then += children in
 // (oz, oy, ox) loop order, then acc / ratio^D (amr.py:254-264).
 template <class T>
-__global__ void __launch_bounds__(kAmrThreads) avgdown_kernel(const DevAvgJob *__restrict__ jobs, int njobs,
+__global__ void __launch_bounds__(kAmrThreads, 4) avgdown_kernel(const DevAvgJob *__restrict__ jobs, int njobs,
                                                               int64_t total, int ncomp, int r0, int r1, int r2,
                                                               T rpow) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     const DevAvgJob &J = jobs[find_job(jobs, njobs, i)];
-    int64_t q = i - J.start;
+    const uint32_t q = (uint32_t)(i - J.start), nx = (uint32_t)J.rn[0], ny = (uint32_t)J.rn[1];
+    const uint32_t t = q / nx;
     int64_t cidx[3];
-    cidx[0] = J.rlo[0] + q % J.rn[0];
-    q /= J.rn[0];
-    cidx[1] = J.rlo[1] + q % J.rn[1];
-    cidx[2] = J.rlo[2] + q / J.rn[1];
+    cidx[0] = J.rlo[0] + (int64_t)(q - t * nx);
+    cidx[1] = J.rlo[1] + (int64_t)(t % ny);
+    cidx[2] = J.rlo[2] + (int64_t)(t / ny);
     const int64_t fsy = J.f.n[0], fsz = J.f.n[0] * J.f.n[1], fsc = fsz * J.f.n[2];
     const int64_t csc = J.c.n[0] * J.c.n[1] * J.c.n[2];
     const int64_t fo = (cidx[0] * r0 - J.f.lo[0]) + (cidx[1] * r1 - J.f.lo[1]) * fsy + (cidx[2] * r2 - J.f.lo[2]) * fsz;
@@ -189,32 +194,94 @@ int64_t floordiv_h(int64_t a, int64_t b) {
   return (q * b > a) ? q - 1 : q;
 }
 
-// stream-ordered upload of a job table, launch, free
-template <class J, class Launch>
-int run_jobs(const std::vector<J> &jobs, int64_t total, void *stream, const char *what, Launch launch) {
-  if (total == 0) return GHX_OK;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  J *dj = nullptr;
-  const size_t bytes = jobs.size() * sizeof(J);
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&dj), bytes, st);
+std::atomic<int64_t> g_amr_launches{0};
+
+}  // namespace
+
+// A prepared transfer: the device job table of one interp / average_down
+// call pattern (fill_patch and average_down cache one per plan), so a call
+// is a single kernel launch with no host-side table work.
+struct ghx_xfer {
+  int kind = 0;  // 0 interp, 1 average_down
+  int device = 0;
+  void *djobs = nullptr;
+  int njobs = 0;
+  int64_t total = 0;
+  int ncomp = 1, r[3] = {1, 1, 1}, spacedim = 3, scheme = 0, elem_bytes = 8;
+  int64_t rpow = 1;
+  int blocks = 0;
+};
+
+namespace {
+
+template <class J>
+int xfer_upload(ghx_xfer *x, const std::vector<J> &jobs, const char *what) {
+  x->njobs = (int)jobs.size();
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, x->device);
+  const int64_t want = (x->total + kAmrThreads - 1) / kAmrThreads;
+  x->blocks = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * 8));
+  if (jobs.empty()) return GHX_OK;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != x->device) cudaSetDevice(x->device);
+  cudaError_t e = cudaMalloc(&x->djobs, jobs.size() * sizeof(J));
+  if (e == cudaSuccess) e = cudaMemcpy(x->djobs, jobs.data(), jobs.size() * sizeof(J), cudaMemcpyHostToDevice);
+  if (prev != x->device) cudaSetDevice(prev);
   if (e != cudaSuccess) return cuda_fail(e, what);
-  e = cudaMemcpyAsync(dj, jobs.data(), bytes, cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess) {
-    int sms = 148, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t want = (total + kAmrThreads - 1) / kAmrThreads;
-    const int blocks = (int)std::min<int64_t>(want, (int64_t)sms * 8);
-    launch(dj, blocks, st);
-    e = cudaGetLastError();
-  }
-  cudaError_t e2 = cudaFreeAsync(dj, st);
-  if (e != cudaSuccess) return cuda_fail(e, what);
-  if (e2 != cudaSuccess) return cuda_fail(e2, what);
   return GHX_OK;
 }
 
-std::atomic<int64_t> g_amr_launches{0};
+int xfer_launch(const ghx_xfer *x, cudaStream_t st) {
+  if (x->total == 0) return GHX_OK;
+  const int nj = x->njobs;
+  if (x->kind == 0) {
+    const DevInterpJob *p = static_cast<const DevInterpJob *>(x->djobs);
+    const bool lin = x->scheme == GHX_INTERP_LINEAR;
+    if (x->elem_bytes == 8) {
+      if (lin)
+        interp_kernel<double, true><<<x->blocks, kAmrThreads, 0, st>>>(p, nj, x->total, x->ncomp, x->r[0], x->r[1],
+                                                                       x->r[2], x->spacedim);
+      else
+        interp_kernel<double, false><<<x->blocks, kAmrThreads, 0, st>>>(p, nj, x->total, x->ncomp, x->r[0], x->r[1],
+                                                                        x->r[2], x->spacedim);
+    } else {
+      if (lin)
+        interp_kernel<float, true><<<x->blocks, kAmrThreads, 0, st>>>(p, nj, x->total, x->ncomp, x->r[0], x->r[1],
+                                                                      x->r[2], x->spacedim);
+      else
+        interp_kernel<float, false><<<x->blocks, kAmrThreads, 0, st>>>(p, nj, x->total, x->ncomp, x->r[0], x->r[1],
+                                                                       x->r[2], x->spacedim);
+    }
+  } else {
+    const DevAvgJob *p = static_cast<const DevAvgJob *>(x->djobs);
+    if (x->elem_bytes == 8)
+      avgdown_kernel<double><<<x->blocks, kAmrThreads, 0, st>>>(p, nj, x->total, x->ncomp, x->r[0], x->r[1], x->r[2],
+                                                                (double)x->rpow);
+    else
+      avgdown_kernel<float><<<x->blocks, kAmrThreads, 0, st>>>(p, nj, x->total, x->ncomp, x->r[0], x->r[1], x->r[2],
+                                                               (float)x->rpow);
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "ghx_xfer_run: launch");
+  g_amr_launches.fetch_add(1);
+  return GHX_OK;
+}
+
+bool check_common(int64_t njobs, const void *jobs, int32_t ncomp, const int32_t *ratio, int32_t spacedim,
+                  int32_t elem_bytes, const char *what) {
+  if ((njobs && !jobs) || njobs < 0 || njobs > (1 << 30) || ncomp < 1 || !ratio || spacedim < 1 || spacedim > 3 ||
+      (elem_bytes != 4 && elem_bytes != 8)) {
+    set_error(std::string(what) + ": bad arguments");
+    return false;
+  }
+  for (int d = 0; d < 3; ++d)
+    if (ratio[d] < 1 || (d >= spacedim && ratio[d] != 1)) {
+      set_error(std::string(what) + ": ratio must be >= 1 (1 on axes >= spacedim)");
+      return false;
+    }
+  return true;
+}
 
 }  // namespace
 
@@ -222,18 +289,13 @@ extern "C" {
 
 int64_t ghx_amr_launch_count(void) { return g_amr_launches.load(); }
 
-int ghx_interp(const ghx_interp_job *jobs, int64_t njobs, int32_t ncomp, const int32_t ratio[3], int32_t spacedim,
-               int32_t scheme, int32_t elem_bytes, void *stream) {
-  if ((njobs && !jobs) || njobs < 0 || njobs > (1 << 30) || ncomp < 1 || !ratio || spacedim < 1 || spacedim > 3 ||
-      (scheme != GHX_INTERP_PC && scheme != GHX_INTERP_LINEAR) || (elem_bytes != 4 && elem_bytes != 8)) {
-    set_error("ghx_interp: bad arguments");
+int ghx_interp_prepare(const ghx_interp_job *jobs, int64_t njobs, int32_t ncomp, const int32_t ratio[3],
+                       int32_t spacedim, int32_t scheme, int32_t elem_bytes, int32_t device, ghx_xfer **out) {
+  if (!out || !check_common(njobs, jobs, ncomp, ratio, spacedim, elem_bytes, "ghx_interp") ||
+      (scheme != GHX_INTERP_PC && scheme != GHX_INTERP_LINEAR)) {
+    if (out && scheme != GHX_INTERP_PC && scheme != GHX_INTERP_LINEAR) set_error("ghx_interp: unknown scheme");
     return GHX_EINVAL;
   }
-  for (int d = 0; d < 3; ++d)
-    if (ratio[d] < 1 || (d >= spacedim && ratio[d] != 1)) {
-      set_error("ghx_interp: ratio must be >= 1 (1 on axes >= spacedim)");
-      return GHX_EINVAL;
-    }
   std::vector<DevInterpJob> dj;
   dj.reserve(njobs);
   int64_t total = 0;
@@ -270,44 +332,42 @@ int ghx_interp(const ghx_interp_job *jobs, int64_t njobs, int32_t ncomp, const i
       d.rn[a] = R[3 + a] - R[a] + 1;
     }
     d.start = total;
+    if (d.rn[0] * d.rn[1] * d.rn[2] >= (1ll << 31) || std::abs(R[0]) >= (1ll << 30) || std::abs(R[3]) >= (1ll << 30) ||
+        std::abs(R[1]) >= (1ll << 30) || std::abs(R[4]) >= (1ll << 30) || std::abs(R[2]) >= (1ll << 30) ||
+        std::abs(R[5]) >= (1ll << 30)) {
+      set_error("ghx_interp: job " + std::to_string(j) + ": region too large (>= 2^31 cells or |index| >= 2^30)");
+      return GHX_EINVAL;
+    }
     total += d.rn[0] * d.rn[1] * d.rn[2];
     dj.push_back(d);
   }
-  const int nj = (int)dj.size();
-  const int r0 = ratio[0], r1 = ratio[1], r2 = ratio[2];
-  int rc = run_jobs(dj, total, stream, "ghx_interp", [&](const DevInterpJob *p, int blocks, cudaStream_t st) {
-    const bool lin = scheme == GHX_INTERP_LINEAR;
-    if (elem_bytes == 8) {
-      if (lin)
-        interp_kernel<double, true><<<blocks, kAmrThreads, 0, st>>>(p, nj, total, ncomp, r0, r1, r2, spacedim);
-      else
-        interp_kernel<double, false><<<blocks, kAmrThreads, 0, st>>>(p, nj, total, ncomp, r0, r1, r2, spacedim);
-    } else {
-      if (lin)
-        interp_kernel<float, true><<<blocks, kAmrThreads, 0, st>>>(p, nj, total, ncomp, r0, r1, r2, spacedim);
-      else
-        interp_kernel<float, false><<<blocks, kAmrThreads, 0, st>>>(p, nj, total, ncomp, r0, r1, r2, spacedim);
-    }
-  });
-  if (rc == GHX_OK && total) g_amr_launches.fetch_add(1);
-  return rc;
+  ghx_xfer *x = new (std::nothrow) ghx_xfer();
+  if (!x) {
+    set_error("ghx_interp: out of memory");
+    return GHX_ENOMEM;
+  }
+  x->kind = 0;
+  x->device = device;
+  x->total = total;
+  x->ncomp = ncomp;
+  for (int d = 0; d < 3; ++d) x->r[d] = ratio[d];
+  x->spacedim = spacedim;
+  x->scheme = scheme;
+  x->elem_bytes = elem_bytes;
+  if (int rc = xfer_upload(x, dj, "ghx_interp_prepare")) {
+    delete x;
+    return rc;
+  }
+  *out = x;
+  return GHX_OK;
 }
 
-int ghx_average_down(const ghx_avgdown_job *jobs, int64_t njobs, int32_t ncomp, const int32_t ratio[3],
-                     int32_t spacedim, int32_t elem_bytes, void *stream) {
-  if ((njobs && !jobs) || njobs < 0 || njobs > (1 << 30) || ncomp < 1 || !ratio || spacedim < 1 || spacedim > 3 ||
-      (elem_bytes != 4 && elem_bytes != 8)) {
-    set_error("ghx_average_down: bad arguments");
+int ghx_average_down_prepare(const ghx_avgdown_job *jobs, int64_t njobs, int32_t ncomp, const int32_t ratio[3],
+                             int32_t spacedim, int32_t elem_bytes, int32_t device, ghx_xfer **out) {
+  if (!out || !check_common(njobs, jobs, ncomp, ratio, spacedim, elem_bytes, "ghx_average_down"))
     return GHX_EINVAL;
-  }
   int64_t rpow = 1;
-  for (int d = 0; d < 3; ++d) {
-    if (ratio[d] < 1 || (d >= spacedim && ratio[d] != 1)) {
-      set_error("ghx_average_down: ratio must be >= 1 (1 on axes >= spacedim)");
-      return GHX_EINVAL;
-    }
-    rpow *= ratio[d];
-  }
+  for (int d = 0; d < 3; ++d) rpow *= ratio[d];
   std::vector<DevAvgJob> dj;
   dj.reserve(njobs);
   int64_t total = 0;
@@ -339,18 +399,75 @@ int ghx_average_down(const ghx_avgdown_job *jobs, int64_t njobs, int32_t ncomp, 
       d.rn[a] = R[3 + a] - R[a] + 1;
     }
     d.start = total;
+    if (d.rn[0] * d.rn[1] * d.rn[2] >= (1ll << 31)) {
+      set_error("ghx_average_down: job " + std::to_string(j) + ": region too large (>= 2^31 cells)");
+      return GHX_EINVAL;
+    }
     total += d.rn[0] * d.rn[1] * d.rn[2];
     dj.push_back(d);
   }
-  const int nj = (int)dj.size();
-  const int r0 = ratio[0], r1 = ratio[1], r2 = ratio[2];
-  int rc = run_jobs(dj, total, stream, "ghx_average_down", [&](const DevAvgJob *p, int blocks, cudaStream_t st) {
-    if (elem_bytes == 8)
-      avgdown_kernel<double><<<blocks, kAmrThreads, 0, st>>>(p, nj, total, ncomp, r0, r1, r2, (double)rpow);
-    else
-      avgdown_kernel<float><<<blocks, kAmrThreads, 0, st>>>(p, nj, total, ncomp, r0, r1, r2, (float)rpow);
-  });
-  if (rc == GHX_OK && total) g_amr_launches.fetch_add(1);
+  ghx_xfer *x = new (std::nothrow) ghx_xfer();
+  if (!x) {
+    set_error("ghx_average_down: out of memory");
+    return GHX_ENOMEM;
+  }
+  x->kind = 1;
+  x->device = device;
+  x->total = total;
+  x->ncomp = ncomp;
+  for (int d = 0; d < 3; ++d) x->r[d] = ratio[d];
+  x->spacedim = spacedim;
+  x->elem_bytes = elem_bytes;
+  x->rpow = rpow;
+  if (int rc = xfer_upload(x, dj, "ghx_average_down_prepare")) {
+    delete x;
+    return rc;
+  }
+  *out = x;
+  return GHX_OK;
+}
+
+int ghx_xfer_run(ghx_xfer *x, void *stream) {
+  if (!x) {
+    set_error("ghx_xfer_run: null handle");
+    return GHX_EINVAL;
+  }
+  return xfer_launch(x, static_cast<cudaStream_t>(stream));
+}
+
+int64_t ghx_xfer_cells(const ghx_xfer *x) { return x ? x->total : 0; }
+
+void ghx_xfer_free(ghx_xfer *x) {
+  if (!x) return;
+  if (x->djobs) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (prev != x->device) cudaSetDevice(x->device);
+    cudaFree(x->djobs);  // synchronising: no launch of this handle is in flight afterwards
+    if (prev != x->device) cudaSetDevice(prev);
+  }
+  delete x;
+}
+
+int ghx_interp(const ghx_interp_job *jobs, int64_t njobs, int32_t ncomp, const int32_t ratio[3], int32_t spacedim,
+               int32_t scheme, int32_t elem_bytes, void *stream) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  ghx_xfer *x = nullptr;
+  if (int rc = ghx_interp_prepare(jobs, njobs, ncomp, ratio, spacedim, scheme, elem_bytes, dev, &x)) return rc;
+  const int rc = ghx_xfer_run(x, stream);
+  ghx_xfer_free(x);
+  return rc;
+}
+
+int ghx_average_down(const ghx_avgdown_job *jobs, int64_t njobs, int32_t ncomp, const int32_t ratio[3],
+                     int32_t spacedim, int32_t elem_bytes, void *stream) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  ghx_xfer *x = nullptr;
+  if (int rc = ghx_average_down_prepare(jobs, njobs, ncomp, ratio, spacedim, elem_bytes, dev, &x)) return rc;
+  const int rc = ghx_xfer_run(x, stream);
+  ghx_xfer_free(x);
   return rc;
 }
 

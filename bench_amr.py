@@ -2,7 +2,7 @@
 rows 1-2): fill_patch (FillBoundary + coarse gather + interpolation) and
 average_down (restriction + ParallelCopy).
 
-    python bench_amr.py [--op fill_patch|average_down] [--steps K] [--warmup W]
+    python bench_amr.py [--op fill_patch|average_down|heat] [--steps K] [--warmup W]
 
 Workload (synthetic, splitmix64 hash data): a 256^3 periodic coarse level
 cut into 64^3 boxes, ncomp 4, float64; the fine level refines the central
@@ -91,7 +91,9 @@ def run(args):
                                   f"[{PATCH_LO},{PATCH_HI}]^3 refined x{RATIO} ({len(fba)} boxes of {BOX}^3, "
                                   f"nghost {NGROW}), ncomp {NCOMP}, float64",
                       "l2": "flushed before every step (512 MiB write + 256 MiB clean read, outside the events)"}}
-    if args.op == "fill_patch":
+    if args.op == "heat":
+        pass
+    elif args.op == "fill_patch":
         call = lambda: A.fill_patch(fine, coarse, fgeom, cgeom, RATIO, A.LINEAR)  # noqa: E731
         t_mean, t_min = timed(call, args.steps, args.warmup, flush, clean)
         ghost_cells = sum(amr.grow(b, NGROW).num_pts - b.num_pts for b in fba)
@@ -132,8 +134,43 @@ def run(args):
                              "frac": round(alg / k_mean / 1e9 / hbm, 4), "unit": "GB/s", "peak_source": peak_src,
                              "kernel_ms": round(k_mean * 1e3, 4)})
         out["cpu_baseline"] = cpu_restrict_sample()
+    if args.op == "heat":
+        out.update(heat_bench(args, amr, cdom, cgeom, cba, flush, clean, hbm, peak_src))
     out["amr_launches"] = int(N.lib.ghx_amr_launch_count())
     print(json.dumps(out), flush=True)
+
+
+def heat_bench(args, amr, cdom, cgeom, cba, flush, clean, hbm, peak_src):
+    """One heat_step (FillBoundary + stencil, the reference demo's single-level
+    loop body) on the coarse layout with ncomp 1, nghost 1; overlap on/off."""
+    from paper_2403_12179_b200 import heat as H
+    dm = amr.DistributionMapping([0] * len(cba))
+    u = amr.MultiFab(cba, dm, 1, 1, cgeom)
+    w = amr.MultiFab(cba, dm, 1, 1, cgeom)
+    u.fill_hash(20261017, cdom)
+    w.setval(0.0)
+    state = {"levels": [(u, w)]}
+    dt, kappa = 1e-6, 1.0
+    res = {}
+    for ov in (True, False):
+        def step(ov=ov):
+            state["levels"] = H.heat_step(state["levels"], [cgeom], dt, kappa, overlap=ov)
+        t_mean, _ = timed(step, args.steps, args.warmup, flush, clean)
+        res["overlap" if ov else "serial"] = round(t_mean * 1e3, 4)
+    cells = sum(b.num_pts for b in cba)
+    xf = H._stencil(state["levels"][0][0], state["levels"][0][1], dt, kappa, cgeom, "all")
+    k_mean, _ = timed(xf.run, args.steps, args.warmup, flush, clean)
+    alg = cells * 16  # read u + write unew, 8 B each (neighbour reads hit L1/L2)
+    return {"metric": "heat_step cells/s (FillBoundary + 7-point stencil, reference demo loop body)",
+            "value": round(cells / (res["serial"] * 1e-3) / 1e9, 3), "unit": "Gcell/s",
+            "ms_per_step": res["serial"], "ms_per_step_overlap": res["overlap"],
+            "config": {"workload": f"{N_CRSE}^3 periodic, {BOX}^3 boxes, ncomp 1, nghost 1, float64 "
+                                   "(the reference heat demo layout)",
+                       "l2": "flushed before every step (512 MiB write + 256 MiB clean read, outside the events)"},
+            "roofline": {"kernel": "advance_kernel<double,3>", "bound": "hbm", "algorithmic_bytes_per_launch": alg,
+                         "achieved": round(alg / k_mean / 1e9, 1), "peak": hbm,
+                         "frac": round(alg / k_mean / 1e9 / hbm, 4), "unit": "GB/s", "peak_source": peak_src,
+                         "kernel_ms": round(k_mean * 1e3, 4)}}
 
 
 def cpu_interp_sample(fine_mf, targets, seconds=5.0):
@@ -177,7 +214,7 @@ def cpu_restrict_sample(seconds=5.0):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--op", default="fill_patch", choices=["fill_patch", "average_down"])
+    ap.add_argument("--op", default="fill_patch", choices=["fill_patch", "average_down", "heat"])
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     args = ap.parse_args()

@@ -221,6 +221,22 @@ int ghx_interp_prepare(const ghx_interp_job *jobs, int64_t njobs, int32_t ncomp,
                        int32_t spacedim, int32_t scheme, int32_t elem_bytes, int32_t device, ghx_xfer **out);
 int ghx_average_down_prepare(const ghx_avgdown_job *jobs, int64_t njobs, int32_t ncomp, const int32_t ratio[3],
                              int32_t spacedim, int32_t elem_bytes, int32_t device, ghx_xfer **out);
+/* One heat-equation step (reference heat.py:172-189) over `region` of each
+ * job: dst = src + sum_d coef[d] * ((src[+e_d] - 2 src) + src[-e_d]) for
+ * d < spacedim, component 0, numpy's operation order (bit-exact).  src must
+ * hold the region grown by one cell (its ghosts filled). */
+typedef struct {
+  const void *src;
+  int64_t src_box[6];
+  void *dst;
+  int64_t dst_box[6];
+  int64_t region[6];
+} ghx_stencil_job;
+#define GHX_ADVANCE_TILES 0 /* 32x8 (x,y) tiles marching z: thick regions */
+#define GHX_ADVANCE_CELLS 1 /* one thread per cell: thin shells */
+int ghx_advance_prepare(const ghx_stencil_job *jobs, int64_t njobs, const double coef[3], int32_t spacedim,
+                        int32_t elem_bytes, int32_t layout, int32_t device, ghx_xfer **out);
+
 int ghx_xfer_run(ghx_xfer *x, void *stream);
 int64_t ghx_xfer_cells(const ghx_xfer *x); /* cells written per run */
 void ghx_xfer_free(ghx_xfer *x);

@@ -126,3 +126,25 @@ def fill_targets(fine_boxes, ngrow, domain, periodic, spacedim):
         if rest:
             out[gi] = rest
     return out
+
+
+def advance(u, u_box, valid_box, coef, spacedim):
+    """heat.py:172-189 on valid_box, component 0: returns the new values
+    (F-order (nx, ny, nz)) in numpy's operation order."""
+    lo = [int(valid_box[d] - u_box[d]) for d in range(3)]
+    hi = [int(valid_box[3 + d] - u_box[d]) + 1 for d in range(3)]
+
+    def at(dx, dy, dz):
+        return u[lo[0] + dx:hi[0] + dx, lo[1] + dy:hi[1] + dy, lo[2] + dz:hi[2] + dz, 0]
+
+    acc = at(0, 0, 0).copy()
+    one = u.dtype.type(coef[0]) if u.dtype == np.float32 else coef[0]
+    if spacedim >= 1:
+        acc += one * (at(1, 0, 0) - 2.0 * at(0, 0, 0) + at(-1, 0, 0))
+    if spacedim >= 2:
+        c = u.dtype.type(coef[1]) if u.dtype == np.float32 else coef[1]
+        acc += c * (at(0, 1, 0) - 2.0 * at(0, 0, 0) + at(0, -1, 0))
+    if spacedim >= 3:
+        c = u.dtype.type(coef[2]) if u.dtype == np.float32 else coef[2]
+        acc += c * (at(0, 0, 1) - 2.0 * at(0, 0, 0) + at(0, 0, -1))
+    return acc

@@ -71,12 +71,14 @@ _SIGS = {
     "ghx_amr_launch_count": (I64, []),
     "ghx_interp_prepare": (C.c_int, [P, I64, I32, PI32, I32, I32, I32, I32, C.POINTER(P)]),
     "ghx_average_down_prepare": (C.c_int, [P, I64, I32, PI32, I32, I32, I32, C.POINTER(P)]),
+    "ghx_advance_prepare": (C.c_int, [P, I64, C.POINTER(C.c_double), I32, I32, I32, I32, C.POINTER(P)]),
     "ghx_xfer_run": (C.c_int, [P, P]),
     "ghx_xfer_cells": (I64, [P]),
     "ghx_xfer_free": (None, [P]),
 }
 
 INTERP_PC, INTERP_LINEAR = 0, 1
+ADVANCE_TILES, ADVANCE_CELLS = 0, 1
 JOB_WORDS = 20  # int64 words per ghx_interp_job / ghx_avgdown_job
 
 EXPORTED = tuple(_SIGS)

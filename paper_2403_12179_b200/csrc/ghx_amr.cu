@@ -1,5 +1,6 @@
 // Coarse/fine level transfers for sm_100a: the two local kernels that
-// fill_patch and average_down run around the exchange engine.
+// fill_patch and average_down run around the exchange engine, plus the heat
+// step's stencil (the consumer the exchange overlaps with).
 //
 //   ghx_interp        interp_box (reference amr.py:269-314): fine cells of a
 //                     region from their coarse parents, piecewise constant
@@ -55,19 +56,6 @@ __device__ __forceinline__ int32_t floordiv32(int32_t a, int32_t b) {
   return (q * b > a) ? q - 1 : q;
 }
 
-template <class J>
-__device__ __forceinline__ int find_job(const J *jobs, int njobs, int64_t i) {
-  int lo = 0, hi = njobs - 1;
-  while (lo < hi) {  // last job with start <= i
-    const int mid = (lo + hi + 1) >> 1;
-    if (jobs[mid].start <= i)
-      lo = mid;
-    else
-      hi = mid - 1;
-  }
-  return lo;
-}
-
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
 __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
@@ -84,15 +72,15 @@ __device__ __forceinline__ float div_rn(float a, float b) { return __fdiv_rn(a, 
 //   v     = T(double(v) + double(slope) * off)   (numpy's float64 loop for
 //                                                 v += slope * off)
 template <class T, bool LINEAR>
-__global__ void __launch_bounds__(kAmrThreads, 3) interp_kernel(const DevInterpJob *__restrict__ jobs, int njobs,
-                                                             int64_t total, int ncomp, int r0, int r1, int r2,
-                                                             int spacedim) {
+__global__ void __launch_bounds__(kAmrThreads, 3) interp_kernel(const DevInterpJob *__restrict__ jobs,
+                                                             const int4 *__restrict__ btasks, int ncomp, int r0,
+                                                             int r1, int r2, int spacedim) {
   const int r[3] = {r0, r1, r2};
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const DevInterpJob &J = jobs[find_job(jobs, njobs, i)];
+  const int4 bt = btasks[blockIdx.x];  // {job, first cell, cells}: one job per block
+  const DevInterpJob &J = jobs[bt.x];
+  for (int k = threadIdx.x; k < bt.z; k += kAmrThreads) {
     // 32-bit index math inside a job (jobs are < 2^31 cells, host-checked)
-    const uint32_t q = (uint32_t)(i - J.start), nx = (uint32_t)J.rn[0], ny = (uint32_t)J.rn[1];
+    const uint32_t q = (uint32_t)(bt.y + k), nx = (uint32_t)J.rn[0], ny = (uint32_t)J.rn[1];
     const uint32_t t = q / nx;
     int32_t fidx[3];
     fidx[0] = (int32_t)J.rlo[0] + (int32_t)(q - t * nx);
@@ -134,13 +122,13 @@ __global__ void __launch_bounds__(kAmrThreads, 3) interp_kernel(const DevInterpJ
 // One thread per coarse cell: acc = child(0,0,0), then += children in
 // (oz, oy, ox) loop order, then acc / ratio^D (amr.py:254-264).
 template <class T>
-__global__ void __launch_bounds__(kAmrThreads, 4) avgdown_kernel(const DevAvgJob *__restrict__ jobs, int njobs,
-                                                              int64_t total, int ncomp, int r0, int r1, int r2,
-                                                              T rpow) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const DevAvgJob &J = jobs[find_job(jobs, njobs, i)];
-    const uint32_t q = (uint32_t)(i - J.start), nx = (uint32_t)J.rn[0], ny = (uint32_t)J.rn[1];
+__global__ void __launch_bounds__(kAmrThreads, 4) avgdown_kernel(const DevAvgJob *__restrict__ jobs,
+                                                              const int4 *__restrict__ btasks, int ncomp, int r0,
+                                                              int r1, int r2, T rpow) {
+  const int4 bt = btasks[blockIdx.x];
+  const DevAvgJob &J = jobs[bt.x];
+  for (int k = threadIdx.x; k < bt.z; k += kAmrThreads) {
+    const uint32_t q = (uint32_t)(bt.y + k), nx = (uint32_t)J.rn[0], ny = (uint32_t)J.rn[1];
     const uint32_t t = q / nx;
     int64_t cidx[3];
     cidx[0] = J.rlo[0] + (int64_t)(q - t * nx);
@@ -166,6 +154,74 @@ __global__ void __launch_bounds__(kAmrThreads, 4) avgdown_kernel(const DevAvgJob
           }
       crse[co + c * csc] = div_rn(acc, rpow);
     }
+  }
+}
+
+// One heat-equation step (reference heat.py:172-189, comp 0):
+//   acc = u;  acc += c_d * ((u[+e_d] - 2*u) + u[-e_d])   for d < DIM
+// in numpy's order, storage type T throughout (coefficients rounded to T).
+// 2.5-D blocking: a block is a 32 x 8 (x, y) tile of one job that marches
+// kAdvZ planes in z, carrying u[z-1], u[z], u[z+1] in registers, so each
+// source value comes from HBM once (x/y neighbours hit L1).
+constexpr int kAdvTX = 32, kAdvTY = 8, kAdvZ = 16;
+
+template <class T, int DIM>
+__global__ void __launch_bounds__(kAmrThreads, 4) advance_kernel(const DevAvgJob *__restrict__ jobs,
+                                                                 const int4 *__restrict__ btasks, T c0, T c1, T c2) {
+  const int4 bt = btasks[blockIdx.x];  // {job, x0 | y0 << 16, z0, nz}
+  const DevAvgJob &J = jobs[bt.x];
+  const int tx = threadIdx.x & (kAdvTX - 1), ty = threadIdx.x / kAdvTX;
+  const int64_t xr = (bt.y & 0xffff) + tx, yr = (bt.y >> 16) + ty;
+  if (xr >= J.rn[0] || yr >= J.rn[1]) return;
+  const int64_t x = J.rlo[0] + xr, y = J.rlo[1] + yr, z = J.rlo[2] + bt.z;
+  const int64_t usy = J.f.n[0], usz = J.f.n[0] * J.f.n[1];
+  const int64_t osy = J.c.n[0], osz = J.c.n[0] * J.c.n[1];
+  const T *u = reinterpret_cast<const T *>(J.fine) + (x - J.f.lo[0]) + (y - J.f.lo[1]) * usy + (z - J.f.lo[2]) * usz;
+  T *o = reinterpret_cast<T *>(J.crse) + (x - J.c.lo[0]) + (y - J.c.lo[1]) * osy + (z - J.c.lo[2]) * osz;
+  T um = DIM >= 3 ? __ldg(u - usz) : T(0);
+  T uc = __ldg(u);
+#pragma unroll 4
+  for (int k = 0; k < bt.w; ++k) {
+    const T up = DIM >= 3 ? __ldg(u + usz) : T(0);
+    const T two_u = mul_rn(T(2), uc);
+    T acc = uc;
+    acc = add_rn(acc, mul_rn(c0, add_rn(sub_rn(__ldg(u + 1), two_u), __ldg(u - 1))));
+    if (DIM >= 2) acc = add_rn(acc, mul_rn(c1, add_rn(sub_rn(__ldg(u + usy), two_u), __ldg(u - usy))));
+    if (DIM >= 3) acc = add_rn(acc, mul_rn(c2, add_rn(sub_rn(up, two_u), um)));
+    *o = acc;
+    um = uc;
+    uc = up;
+    u += usz;
+    o += osz;
+  }
+}
+
+// The same stencil, one thread per cell of a flat cell list (block tasks of
+// kAmrThreads * 4 cells of one job): for the thin one-cell shells of the
+// overlapped heat step, where 32 x 8 tiles would idle most lanes.
+template <class T, int DIM>
+__global__ void __launch_bounds__(kAmrThreads, 4) advance_flat_kernel(const DevAvgJob *__restrict__ jobs,
+                                                                      const int4 *__restrict__ btasks, T c0, T c1,
+                                                                      T c2) {
+  const int4 bt = btasks[blockIdx.x];
+  const DevAvgJob &J = jobs[bt.x];
+  for (int k = threadIdx.x; k < bt.z; k += kAmrThreads) {
+    const uint32_t q = (uint32_t)(bt.y + k), nx = (uint32_t)J.rn[0], ny = (uint32_t)J.rn[1];
+    const uint32_t t = q / nx;
+    const int64_t x = J.rlo[0] + (int64_t)(q - t * nx), y = J.rlo[1] + (int64_t)(t % ny),
+                  z = J.rlo[2] + (int64_t)(t / ny);
+    const int64_t usy = J.f.n[0], usz = J.f.n[0] * J.f.n[1];
+    const T *u = reinterpret_cast<const T *>(J.fine) + (x - J.f.lo[0]) + (y - J.f.lo[1]) * usy +
+                 (z - J.f.lo[2]) * usz;
+    T *o = reinterpret_cast<T *>(J.crse) + (x - J.c.lo[0]) + (y - J.c.lo[1]) * J.c.n[0] +
+           (z - J.c.lo[2]) * J.c.n[0] * J.c.n[1];
+    const T uc = __ldg(u);
+    const T two_u = mul_rn(T(2), uc);
+    T acc = uc;
+    acc = add_rn(acc, mul_rn(c0, add_rn(sub_rn(__ldg(u + 1), two_u), __ldg(u - 1))));
+    if (DIM >= 2) acc = add_rn(acc, mul_rn(c1, add_rn(sub_rn(__ldg(u + usy), two_u), __ldg(u - usy))));
+    if (DIM >= 3) acc = add_rn(acc, mul_rn(c2, add_rn(sub_rn(__ldg(u + usz), two_u), __ldg(u - usz))));
+    *o = acc;
   }
 }
 
@@ -202,64 +258,113 @@ std::atomic<int64_t> g_amr_launches{0};
 // call pattern (fill_patch and average_down cache one per plan), so a call
 // is a single kernel launch with no host-side table work.
 struct ghx_xfer {
-  int kind = 0;  // 0 interp, 1 average_down
+  int kind = 0;  // 0 interp, 1 average_down, 2 stencil (tiles), 3 stencil (flat cells)
   int device = 0;
   void *djobs = nullptr;
+  int4 *dtasks = nullptr;  // one block per task: {job, ...}
+  int ntasks = 0;
   int njobs = 0;
   int64_t total = 0;
   int ncomp = 1, r[3] = {1, 1, 1}, spacedim = 3, scheme = 0, elem_bytes = 8;
   int64_t rpow = 1;
+  double coef[3] = {0, 0, 0};  // advance: dt * diffusivity / dx_d^2
   int blocks = 0;
 };
 
 namespace {
 
+constexpr int kCellsPerBlock = kAmrThreads * 4;
+
+// Block tasks: interp / average_down blocks take kCellsPerBlock consecutive
+// cells of one job; the stencil takes 32 x 8 x kAdvZ tiles of one job.
+template <class J>
+std::vector<int4> block_tasks(const ghx_xfer *x, const std::vector<J> &jobs) {
+  std::vector<int4> t;
+  for (size_t j = 0; j < jobs.size(); ++j) {
+    const J &d = jobs[j];
+    if (x->kind == 2) {  // 32 x 8 x kAdvZ tiles
+      for (int64_t z0 = 0; z0 < d.rn[2]; z0 += kAdvZ)
+        for (int64_t y0 = 0; y0 < d.rn[1]; y0 += kAdvTY)
+          for (int64_t x0 = 0; x0 < d.rn[0]; x0 += kAdvTX)
+            t.push_back(make_int4((int)j, (int)(x0 | (y0 << 16)), (int)z0, (int)std::min<int64_t>(kAdvZ, d.rn[2] - z0)));
+    } else {
+      const int64_t cells = d.rn[0] * d.rn[1] * d.rn[2];
+      for (int64_t c0 = 0; c0 < cells; c0 += kCellsPerBlock)
+        t.push_back(make_int4((int)j, (int)c0, (int)std::min<int64_t>(kCellsPerBlock, cells - c0), 0));
+    }
+  }
+  return t;
+}
+
 template <class J>
 int xfer_upload(ghx_xfer *x, const std::vector<J> &jobs, const char *what) {
   x->njobs = (int)jobs.size();
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, x->device);
-  const int64_t want = (x->total + kAmrThreads - 1) / kAmrThreads;
-  x->blocks = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * 8));
   if (jobs.empty()) return GHX_OK;
+  for (const J &d : jobs)
+    if (x->kind == 2 && (d.rn[0] >= 65536 || d.rn[1] >= 32768)) {
+      set_error(std::string(what) + ": stencil region extent too large (x < 65536, y < 32768)");
+      return GHX_EINVAL;
+    }
+  const std::vector<int4> tasks = block_tasks(x, jobs);
+  x->ntasks = (int)tasks.size();
+  x->blocks = x->ntasks;
   int prev = 0;
   cudaGetDevice(&prev);
   if (prev != x->device) cudaSetDevice(x->device);
   cudaError_t e = cudaMalloc(&x->djobs, jobs.size() * sizeof(J));
   if (e == cudaSuccess) e = cudaMemcpy(x->djobs, jobs.data(), jobs.size() * sizeof(J), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMalloc(&x->dtasks, tasks.size() * sizeof(int4));
+  if (e == cudaSuccess) e = cudaMemcpy(x->dtasks, tasks.data(), tasks.size() * sizeof(int4), cudaMemcpyHostToDevice);
   if (prev != x->device) cudaSetDevice(prev);
   if (e != cudaSuccess) return cuda_fail(e, what);
   return GHX_OK;
 }
 
 int xfer_launch(const ghx_xfer *x, cudaStream_t st) {
-  if (x->total == 0) return GHX_OK;
-  const int nj = x->njobs;
+  if (x->total == 0 || x->ntasks == 0) return GHX_OK;
   if (x->kind == 0) {
     const DevInterpJob *p = static_cast<const DevInterpJob *>(x->djobs);
     const bool lin = x->scheme == GHX_INTERP_LINEAR;
     if (x->elem_bytes == 8) {
       if (lin)
-        interp_kernel<double, true><<<x->blocks, kAmrThreads, 0, st>>>(p, nj, x->total, x->ncomp, x->r[0], x->r[1],
+        interp_kernel<double, true><<<x->blocks, kAmrThreads, 0, st>>>(p, x->dtasks, x->ncomp, x->r[0], x->r[1],
                                                                        x->r[2], x->spacedim);
       else
-        interp_kernel<double, false><<<x->blocks, kAmrThreads, 0, st>>>(p, nj, x->total, x->ncomp, x->r[0], x->r[1],
+        interp_kernel<double, false><<<x->blocks, kAmrThreads, 0, st>>>(p, x->dtasks, x->ncomp, x->r[0], x->r[1],
                                                                         x->r[2], x->spacedim);
     } else {
       if (lin)
-        interp_kernel<float, true><<<x->blocks, kAmrThreads, 0, st>>>(p, nj, x->total, x->ncomp, x->r[0], x->r[1],
+        interp_kernel<float, true><<<x->blocks, kAmrThreads, 0, st>>>(p, x->dtasks, x->ncomp, x->r[0], x->r[1],
                                                                       x->r[2], x->spacedim);
       else
-        interp_kernel<float, false><<<x->blocks, kAmrThreads, 0, st>>>(p, nj, x->total, x->ncomp, x->r[0], x->r[1],
+        interp_kernel<float, false><<<x->blocks, kAmrThreads, 0, st>>>(p, x->dtasks, x->ncomp, x->r[0], x->r[1],
                                                                        x->r[2], x->spacedim);
     }
+  } else if (x->kind == 2 || x->kind == 3) {
+    const DevAvgJob *p = static_cast<const DevAvgJob *>(x->djobs);
+    const double *c = x->coef;
+#define GHX_ADV(T, D)                                                                                        \
+  if (x->kind == 2)                                                                                          \
+    advance_kernel<T, D><<<x->blocks, kAmrThreads, 0, st>>>(p, x->dtasks, (T)c[0], (T)c[1], (T)c[2]);        \
+  else                                                                                                       \
+    advance_flat_kernel<T, D><<<x->blocks, kAmrThreads, 0, st>>>(p, x->dtasks, (T)c[0], (T)c[1], (T)c[2])
+    if (x->elem_bytes == 8) {
+      if (x->spacedim == 1) GHX_ADV(double, 1);
+      else if (x->spacedim == 2) GHX_ADV(double, 2);
+      else GHX_ADV(double, 3);
+    } else {
+      if (x->spacedim == 1) GHX_ADV(float, 1);
+      else if (x->spacedim == 2) GHX_ADV(float, 2);
+      else GHX_ADV(float, 3);
+    }
+#undef GHX_ADV
   } else {
     const DevAvgJob *p = static_cast<const DevAvgJob *>(x->djobs);
     if (x->elem_bytes == 8)
-      avgdown_kernel<double><<<x->blocks, kAmrThreads, 0, st>>>(p, nj, x->total, x->ncomp, x->r[0], x->r[1], x->r[2],
+      avgdown_kernel<double><<<x->blocks, kAmrThreads, 0, st>>>(p, x->dtasks, x->ncomp, x->r[0], x->r[1], x->r[2],
                                                                 (double)x->rpow);
     else
-      avgdown_kernel<float><<<x->blocks, kAmrThreads, 0, st>>>(p, nj, x->total, x->ncomp, x->r[0], x->r[1], x->r[2],
+      avgdown_kernel<float><<<x->blocks, kAmrThreads, 0, st>>>(p, x->dtasks, x->ncomp, x->r[0], x->r[1], x->r[2],
                                                                (float)x->rpow);
   }
   cudaError_t e = cudaGetLastError();
@@ -427,6 +532,72 @@ int ghx_average_down_prepare(const ghx_avgdown_job *jobs, int64_t njobs, int32_t
   return GHX_OK;
 }
 
+int ghx_advance_prepare(const ghx_stencil_job *jobs, int64_t njobs, const double coef[3], int32_t spacedim,
+                        int32_t elem_bytes, int32_t layout, int32_t device, ghx_xfer **out) {
+  if (layout != GHX_ADVANCE_TILES && layout != GHX_ADVANCE_CELLS) {
+    set_error("ghx_advance: layout must be GHX_ADVANCE_TILES or GHX_ADVANCE_CELLS");
+    return GHX_EINVAL;
+  }
+  const int32_t one[3] = {1, 1, 1};
+  if (!out || !coef || !check_common(njobs, jobs, 1, one, spacedim, elem_bytes, "ghx_advance")) return GHX_EINVAL;
+  std::vector<DevAvgJob> dj;
+  dj.reserve(njobs);
+  int64_t total = 0;
+  for (int64_t j = 0; j < njobs; ++j) {
+    const ghx_stencil_job &J = jobs[j];
+    const int64_t *R = J.region;
+    if (R[3] < R[0] || R[4] < R[1] || R[5] < R[2]) continue;
+    int64_t glo[3], ghi[3];  // the stencil reads one cell around the region on axes < spacedim
+    for (int d = 0; d < 3; ++d) {
+      glo[d] = R[d] - (d < spacedim ? 1 : 0);
+      ghi[d] = R[3 + d] + (d < spacedim ? 1 : 0);
+    }
+    if (!inside(J.src_box, glo, ghi) || !inside(J.dst_box, R, R + 3)) {
+      set_error("ghx_advance: job " + std::to_string(j) + ": region (grown by 1) outside the source or "
+                "destination fab");
+      return GHX_EINVAL;
+    }
+    if (!J.src || !J.dst) {
+      set_error("ghx_advance: null fab pointer");
+      return GHX_EINVAL;
+    }
+    DevAvgJob d;
+    std::memset(&d, 0, sizeof(d));
+    d.fine = reinterpret_cast<uint64_t>(J.src);
+    d.crse = reinterpret_cast<uint64_t>(J.dst);
+    d.f = geo(J.src_box);
+    d.c = geo(J.dst_box);
+    for (int a = 0; a < 3; ++a) {
+      d.rlo[a] = R[a];
+      d.rn[a] = R[3 + a] - R[a] + 1;
+    }
+    d.start = total;
+    if (d.rn[0] * d.rn[1] * d.rn[2] >= (1ll << 31)) {
+      set_error("ghx_advance: job " + std::to_string(j) + ": region too large (>= 2^31 cells)");
+      return GHX_EINVAL;
+    }
+    total += d.rn[0] * d.rn[1] * d.rn[2];
+    dj.push_back(d);
+  }
+  ghx_xfer *x = new (std::nothrow) ghx_xfer();
+  if (!x) {
+    set_error("ghx_advance: out of memory");
+    return GHX_ENOMEM;
+  }
+  x->kind = layout == GHX_ADVANCE_TILES ? 2 : 3;
+  x->device = device;
+  x->total = total;
+  x->spacedim = spacedim;
+  x->elem_bytes = elem_bytes;
+  for (int d = 0; d < 3; ++d) x->coef[d] = coef[d];
+  if (int rc = xfer_upload(x, dj, "ghx_advance_prepare")) {
+    delete x;
+    return rc;
+  }
+  *out = x;
+  return GHX_OK;
+}
+
 int ghx_xfer_run(ghx_xfer *x, void *stream) {
   if (!x) {
     set_error("ghx_xfer_run: null handle");
@@ -444,6 +615,7 @@ void ghx_xfer_free(ghx_xfer *x) {
     cudaGetDevice(&prev);
     if (prev != x->device) cudaSetDevice(x->device);
     cudaFree(x->djobs);  // synchronising: no launch of this handle is in flight afterwards
+    if (x->dtasks) cudaFree(x->dtasks);
     if (prev != x->device) cudaSetDevice(prev);
   }
   delete x;

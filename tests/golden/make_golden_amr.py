@@ -241,11 +241,79 @@ def gen_fill_patch(rng, n):
                    [True, True], amr.LINEAR, np.float64)
 
 
+# ------------------------------------------------------------- heat step loop
+
+def run_heat(name, dim, cext, cmgs, fine_boxes, ratio, nranks, steps, dt, diffusivity, dtype):
+    """The reference demo's loop body (heat.py:264-273) for ``steps`` steps."""
+    from miniamr_core.heat import _advance_level
+    set_cfg(dim, dtype)
+    cdom = Box([0] * dim, [e - 1 for e in cext])
+    cgeom = Geometry(cdom, [0.0] * dim, [1.0] * dim, [True] * dim)
+    fgeom = cgeom.refined(ratio)
+    cba = decompose(cdom, cmgs)
+    cdm = DistributionMapping([i % nranks for i in range(len(cba))], nranks)
+    fba = BoxArray(fine_boxes) if fine_boxes else None
+    fdm = DistributionMapping([(i + 1) % nranks for i in range(len(fba))], nranks) if fba else None
+    geoms = [cgeom, fgeom]
+
+    def program(ctx):
+        levels = []
+        for lv, (ba, dm, geom) in enumerate([(cba, cdm, cgeom)] + ([(fba, fdm, fgeom)] if fba else [])):
+            u = MultiFab(ba, dm, 1, 1, geom=geom)
+            w = MultiFab(ba, dm, 1, 1, geom=geom)
+            for gi in u.local_indices:
+                fill(u.fabs[gi], ba[gi], geom.domain, inputs.SEED + lv)
+            w.setval(0.0)
+            levels.append((u, w))
+        ctx.barrier()
+        be = Backend("serial")
+        for _ in range(steps):
+            comm.fill_boundary(levels[0][0], geoms[0], backend=be)
+            if len(levels) > 1:
+                amr.fill_patch(levels[1][0], levels[0][0], geoms[1], geoms[0], ratio, amr.LINEAR, backend=be)
+            for lv, (u, w) in enumerate(levels):
+                _advance_level(u, w, dt, diffusivity, geoms[lv], be)
+            if len(levels) > 1:
+                amr.average_down(levels[1][1], levels[0][1], ratio, be)
+            levels = [(w, u) for (u, w) in levels]
+        out = {}
+        for lv, (u, w) in enumerate(levels):
+            for gi in u.local_indices:
+                out[(lv, "u", gi)] = inputs.bits(u.fabs[gi].data).copy(order="F")
+                out[(lv, "w", gi)] = inputs.bits(w.fabs[gi].data).copy(order="F")
+        return out
+
+    for out in comm.runtime_spawn(nranks, program):
+        for (lv, which, gi), a in out.items():
+            ARRAYS[f"{name}/l{lv}{which}{gi}"] = a
+    CASES.append(dict(name=name, kind="heat", dim=dim, cext=pad3(cext, 1), cmgs=cmgs,
+                      fine_boxes=[box6(b) for b in (fine_boxes or [])], ratio=ratio, nranks=nranks, steps=steps,
+                      dt=dt, diffusivity=diffusivity, dtype=np.dtype(dtype).name,
+                      crse_boxes=[box6(b) for b in cba], crse_rank=list(cdm.rank_of),
+                      fine_rank=list(fdm.rank_of) if fdm else []))
+    reset_cfg()
+
+
+def gen_heat(rng):
+    run_heat("heat_1l_2d", 2, [16, 16], 8, None, 2, 1, 3, 1e-4, 1.0, np.float64)
+    run_heat("heat_1l_3d_2r", 3, [12, 12, 12], 6, None, 2, 2, 2, 2e-5, 0.7, np.float64)
+    run_heat("heat_1l_3d_f32", 3, [8, 8, 8], 4, None, 2, 1, 2, 1e-4, 1.0, np.float32)
+    run_heat("heat_1l_1d", 1, [32], 8, None, 2, 2, 4, 1e-4, 1.0, np.float64)
+    config.set_spacedim(2)
+    run_heat("heat_2l_2d", 2, [16, 16], 8, [Box((8, 8), (23, 23))], 2, 1, 2, 2e-5, 1.0, np.float64)
+    config.set_spacedim(2)
+    run_heat("heat_2l_2d_2r", 2, [16, 16], 8, [Box((4, 8), (15, 23)), Box((16, 8), (27, 19))], 2, 2, 2, 2e-5,
+             1.0, np.float64)
+    config.set_spacedim(3)
+    run_heat("heat_2l_3d", 3, [8, 8, 8], 4, [Box((4, 4, 4), (11, 11, 11))], 2, 2, 2, 1e-5, 1.0, np.float64)
+
+
 def main():
     rng = np.random.default_rng(20261017)
     gen_interp(rng, 30)
     gen_avgdown(rng, 18)
     gen_fill_patch(rng, 18)
+    gen_heat(rng)
     with open(os.path.join(HERE, "golden_amr.json"), "w") as f:
         json.dump({"generator": "tests/golden/make_golden_amr.py", "reference": "miniamr_core (amr.py)",
                    "seed_fine": inputs.SEED, "seed_crse": SEED_C, "cases": CASES}, f, indent=0)

@@ -131,6 +131,12 @@ int ghx_exec_buffer_elems(const ghx_exec *ex, int64_t *per_peer);
  * pairs, tags in sector-swap pairs, grid blocks, load flavour. */
 int ghx_exec_detail(const ghx_exec *ex, int64_t out[8]);
 
+/* Seam-chunk ("ring") tasks for x-face sector swaps of periodic x-lines:
+ * each 64-byte row seam is read and written with one coalesced access
+ * (fewer, larger transactions: meant for fabs in host memory over PCIe;
+ * on HBM the sector-swap chains are faster).  Only before the first run. */
+int ghx_exec_set_ring(ghx_exec *ex, int32_t on);
+
 /* Launch-time tuning knob (warps per block * blocks): 0 = default. */
 int ghx_exec_set_grid(ghx_exec *ex, int32_t blocks, int32_t threads);
 

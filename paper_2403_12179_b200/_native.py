@@ -50,6 +50,7 @@ _SIGS = {
     "ghx_exec_buffer_elems": (C.c_int, [P, PI64]),
     "ghx_exec_detail": (C.c_int, [P, PI64]),
     "ghx_exec_set_grid": (C.c_int, [P, I32, I32]),
+    "ghx_exec_set_ring": (C.c_int, [P, I32]),
     "ghx_device_alloc": (C.c_int, [I32, C.c_size_t, C.POINTER(P)]),
     "ghx_device_free": (C.c_int, [P]),
     "ghx_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(P)]),

@@ -412,13 +412,16 @@ class CommPlan:
         return {s: segs for (s, d), segs in sorted(self.pair_segments.items()) if d == rank}
 
     def executor(self, rank, kind, src_mf, dst_mf, scomp, dcomp, ncomp) -> "Executor":
+        # fabs in pinned host memory: seam-chunk (ring) tasks, fewer and larger PCIe transactions
+        host = getattr(dst_mf, "memory", "device") == "pinned" or getattr(src_mf, "memory", "device") == "pinned"
+        ring = {"1": True, "0": False}.get(os.environ.get("GHX_RING", ""), host)
         key = (rank, kind, src_mf.ngrow.comps, src_mf.ncomp, dst_mf.ngrow.comps, dst_mf.ncomp,
-               scomp, dcomp, ncomp, dst_mf.dtype.itemsize, dst_mf.device)
+               scomp, dcomp, ncomp, dst_mf.dtype.itemsize, dst_mf.device, ring)
         with self._lock:
             ex = self._execs.get(key)
             if ex is None:
                 ex = Executor(self, rank, kind, src_mf.storage_rows(), src_mf.ncomp, dst_mf.storage_rows(),
-                              dst_mf.ncomp, scomp, dcomp, ncomp, dst_mf.dtype.itemsize, dst_mf.device)
+                              dst_mf.ncomp, scomp, dcomp, ncomp, dst_mf.dtype.itemsize, dst_mf.device, ring)
                 self._execs[key] = ex
         return ex
 
@@ -436,11 +439,14 @@ class Executor:
     """One rank's compiled share of a plan for one storage layout (a device
     tag table; ``run`` is one launch of the fused copy kernel)."""
 
-    def __init__(self, plan, rank, kind, src_rows, src_nc, dst_rows, dst_nc, scomp, dcomp, ncomp, item, device):
+    def __init__(self, plan, rank, kind, src_rows, src_nc, dst_rows, dst_nc, scomp, dcomp, ncomp, item, device,
+                 ring=False):
         h = C.c_void_p()
         N.check(N.lib.ghx_exec_create(plan._h, rank, kind, N.i64p(src_rows), src_nc, N.i64p(dst_rows), dst_nc,
                                       scomp, dcomp, ncomp, item, device, C.byref(h)))
         self._h = h
+        if ring:
+            N.check(N.lib.ghx_exec_set_ring(h, 1))
         self.plan = plan
         self.nsrc = len(src_rows)
         self.ndst = len(dst_rows)

@@ -293,6 +293,89 @@ __device__ __forceinline__ void chain_task(const DevTag *__restrict__ tags, cons
   }
 }
 
+// A ring task runs the x-face sector swaps of a periodic x-line of k fabs
+// F_0..F_{k-1} (ring tags T_j: F_j's last sector <-> F_{j+1}'s first
+// sector, all with the same row geometry) as *seam chunks*: the last
+// sector of row y and the first sector of row y+1 of a fab are adjacent
+// 64 bytes, so a lane pair owns a chunk and reads and writes it with one
+// coalesced 64-byte access each (the swap form needs two 32-byte reads and
+// two writes to different fabs; over PCIe the transaction count is the
+// cost, scripts/microbench/pcie_probe.cu).  Lane pair p = (fab j = p % k,
+// stream s = p / k); a stream walks one (z, comp) column of the tag's rows.
+// Per column, chunk c = (S0 row c, S1 row c+1), c = -1 .. ny-1, where S0 =
+// a fab's last sector (hi valid | hi ghost) and S1 = its first sector (lo
+// ghost | lo valid).  New contents (x-ring neighbours, same row y):
+//   S0(j, y) = [S0(j, y).lo | S1(j+1, y).hi],  S1(j, y) = [S0(j-1, y).lo | S1(j, y).hi]
+// At step c a lane loads its sector of chunk c, receives its neighbour half
+// with one shuffle and writes its sector of chunk c-1 (side 0 waits for
+// S1(j+1, c-1), loaded two steps earlier; side 1 for S0(j-1, c), loaded
+// this step).  Every sector is loaded before it is stored, so loads are
+// issued kRingAhead steps ahead.  A task covers kRingRows rows: the rows
+// each side writes are exactly the rows it loads, so tasks need no halo.
+constexpr int kRingAhead = 2;
+constexpr int kRingRows = 16;  // rows per ring task (a task writes rows [y0, y0 + kRingRows) of its columns)
+
+template <int LD>
+__device__ __forceinline__ void ring_task(const DevTag *__restrict__ tags, const int *__restrict__ ring, int off,
+                                          int kw, int q0, int lane) {
+  const int k = kw & 31, y0 = (kw >> 5) * kRingRows;
+  const int p = lane >> 1, side = lane & 1;
+  const int j = p % k, sidx = p / k;
+  const int jn = (j + 1) % k, jp = (j + k - 1) % k;
+  // my sector's tag: side 0 = T_j's source (F_j last sector), side 1 = T_{j-1}'s destination (F_j first sector)
+  const DevTag &t = tags[__ldg(ring + off + (side ? jp : j))];
+  const char *base = reinterpret_cast<const char *>(side ? __ldg(&t.dst) : __ldg(&t.src));
+  const int64_t sy = side ? __ldg(&t.dst_sy) : __ldg(&t.src_sy);
+  const int64_t sz = side ? __ldg(&t.dst_sz) : __ldg(&t.src_sz);
+  const int64_t sc = side ? __ldg(&t.dst_sc) : __ldg(&t.src_sc);
+  const int ny_tag = (int)__ldg(&t.ny), nz = (int)__ldg(&t.nz);
+  const int ncol = (int)(__ldg(&t.nvec) / (uint32_t)(ny_tag * nz));
+  const int y1 = min(ny_tag, y0 + kRingRows);  // rows [y0, y1) of this task
+  const int q = q0 + sidx;
+  const bool active = sidx < (32 / (2 * k)) && q < nz * ncol;
+  const int src = side ? 2 * (jp + k * sidx) : 2 * (jn + k * sidx) + 1;  // whose half I receive
+  const char *col = base + ((((int64_t)(q % nz)) * sz + (int64_t)(q / max(nz, 1)) * sc) << 4);
+  // row r of my sector: side 0 holds row c at step c, side 1 holds row c+1
+  auto addr = [&](int r) { return const_cast<char *>(col + (((int64_t)r * sy) << 4)); };
+  auto my_row = [&](int c) { return side ? c + 1 : c; };
+  auto loadable = [&](int c) { const int r = my_row(c); return active && r >= y0 && r < y1; };
+  // loads stay whole 32-byte sectors (one coalesced 64-byte access per lane
+  // pair); each side keeps only the half it needs: side 0 the low half of
+  // its S0 (valid, kept), side 1 the high half of its S1 (valid, kept)
+  u8x32 pre[kRingAhead + 1];
+  uint4 h0 = make_uint4(0, 0, 0, 0), h1 = h0, h2 = h0;
+#pragma unroll
+  for (int a = 0; a <= kRingAhead; ++a) {
+    const int c = y0 - 1 + a;
+    if (loadable(c)) pre[a] = ld32<LD>(addr(my_row(c)));
+  }
+#pragma unroll 1
+  for (int c = y0 - 1; c <= y1; ++c) {
+    h2 = h1;
+    h1 = h0;
+    h0 = side ? make_uint4(pre[0].w[4], pre[0].w[5], pre[0].w[6], pre[0].w[7])
+              : make_uint4(pre[0].w[0], pre[0].w[1], pre[0].w[2], pre[0].w[3]);
+#pragma unroll
+    for (int a = 0; a < kRingAhead; ++a) pre[a] = pre[a + 1];
+    if (loadable(c + kRingAhead + 1)) pre[kRingAhead] = ld32<LD>(addr(my_row(c + kRingAhead + 1)));
+    // side 0 gives its S0 row c low half (to side 1 of F_{j+1}); side 1 gives
+    // its S1 row c-1 high half (to side 0 of F_{j-1})
+    const uint4 give = side ? h2 : h0;
+    uint4 got;
+    got.x = __shfl_sync(0xffffffffu, give.x, src);
+    got.y = __shfl_sync(0xffffffffu, give.y, src);
+    got.z = __shfl_sync(0xffffffffu, give.z, src);
+    got.w = __shfl_sync(0xffffffffu, give.w, src);
+    if (!active) continue;
+    const int r = side ? c : c - 1;  // side 0 writes S0 row c-1, side 1 writes S1 row c
+    if (r >= y0 && r < y1) {
+      const uint4 lo = side ? got : h1, hi = side ? h1 : got;
+      const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+      st32(addr(r), w);
+    }
+  }
+}
+
 // cooperative 112-byte descriptor load into this warp's shared slot
 __device__ __forceinline__ void fetch_tag(const DevTag *__restrict__ tags, int idx, DevTag *slot, int lane) {
   if (lane < kTagVec)
@@ -315,7 +398,7 @@ __global__ void ghx_bind_kernel(DevTag *tags, int ntags, void *const *__restrict
 // per-executor counter (counter[0]); every warp counts itself out in
 // counter[1] and the last one resets both, so the next launch (stream
 // ordered) starts from zero without a memset.  Heavy tasks come first.
-template <int LD>
+template <int LD, bool RING = false>
 __global__ void __launch_bounds__(kThreads, GHX_MINB) ghx_copy_kernel(const DevTag *__restrict__ tags,
                                                             const int4 *__restrict__ tasks, int ntasks,
                                                             const int *__restrict__ chains,
@@ -345,6 +428,8 @@ __global__ void __launch_bounds__(kThreads, GHX_MINB) ghx_copy_kernel(const DevT
       const int4 nxt = (w + 1 < last) ? __ldg(tasks + w + 1) : tk;
       if (tk.z == -3) {  // chain task: all seams of one chain, kChainRows rows
         chain_task<LD>(tags, chains, tk.x, tk.w, (uint32_t)tk.y, kChainRows, lane);
+      } else if (RING && tk.z == -4) {  // ring task: seam chunks of 32/(2k) columns of one x-ring
+        ring_task<LD>(tags, chains, tk.x, tk.w, tk.y, lane);
       } else if (tk.z == -2) {  // sector-swap task over one chunk of T1
         const int sl = tk.x & (kSwapSlots - 1);
         if (swc_id[wib][sl] != tk.x) {
@@ -462,6 +547,8 @@ struct ghx_exec {
   int ld_mode = 2;  // ld.global.cg measured best on B200 (see profiles/)
   int64_t elems = 0;
   int64_t npaired = 0, nswap = 0;
+  bool ring = false;    // x-face seams as ring tasks (coalesced 64-B chunks)
+  int64_t nring = 0;
   std::vector<uint8_t> swap_fab;  // fabs touched by sector-swap tasks
   std::vector<int64_t> buf_elems;  // per peer (pack: send, unpack: recv)
   std::vector<DevTag> htags;
@@ -566,6 +653,40 @@ int swap_low(const ghx_exec *ex, int ia, int ib) {
   return -1;
 }
 
+// Order the sector-swap tags of one chain of fabs as an x-ring for
+// ring_task: T_j moves F_j's last sector <-> F_{j+1}'s first sector, every
+// fab appears once on each side, the ring closes, and for every fab the
+// first sector of row y+1 directly follows the last sector of row y (seam
+// chunks are 64 contiguous bytes).  Returns {} if the chain is not such a
+// ring (then chain / swap tasks are used).
+std::vector<int32_t> ring_order(const ghx_exec *ex, const std::vector<int32_t> &ts) {
+  const int k = (int)ts.size();
+  if (k < 1 || k > 16) return {};
+  std::map<int32_t, int32_t> by_src;  // source fab (L) -> tag
+  for (int32_t t : ts)
+    if (!by_src.emplace(std::get<0>(ex->hkeys[t]), t).second) return {};
+  std::vector<int32_t> order;
+  int32_t t = ts[0];
+  for (int n = 0; n < k; ++n) {
+    order.push_back(t);
+    auto it = by_src.find(std::get<1>(ex->hkeys[t]));  // next fab's tag
+    if (it == by_src.end()) return {};
+    t = it->second;
+  }
+  if (t != ts[0]) return {};
+  std::vector<int32_t> seen(order);
+  std::sort(seen.begin(), seen.end());
+  if (std::unique(seen.begin(), seen.end()) != seen.end()) return {};
+  for (int j = 0; j < k; ++j) {
+    const DevTag &a = ex->htags[order[(j + k - 1) % k]];  // its dst = F_j's first sector
+    const DevTag &b = ex->htags[order[j]];                // its src = F_j's last sector
+    if (a.ny != b.ny || a.nz != b.nz || a.nvec != b.nvec || a.dst_sy != b.src_sy || a.dst_sz != b.src_sz ||
+        a.dst_sc != b.src_sc || a.dst_off + a.dst_sy != b.src_off + 2 || a.ny < 1)
+      return {};
+  }
+  return order;
+}
+
 // Warp tasks.  Mirror tags (src<->dst swapped, opposite shift, same shape)
 // are paired chunk by chunk so the two halves of every shared sector move
 // together; everything else pairs consecutive chunks of one tag.
@@ -591,6 +712,9 @@ void build_tasks(ghx_exec *ex) {
   std::vector<int4> loc, rem, swaps;
   ex->npaired = 0;
   ex->nswap = 0;
+  ex->nring = 0;
+  ex->hchain.clear();
+  ex->swap_fab.clear();
   const bool allow_swap = std::getenv("GHX_NO_SWAP") == nullptr;
   std::vector<int32_t> swap_lo;  // low tag of every sector-swap pair
   for (size_t i = 0; i < n; ++i) {
@@ -638,11 +762,28 @@ void build_tasks(ghx_exec *ex) {
     std::map<int32_t, std::vector<int32_t>> chains;
     for (int32_t t : swap_lo) chains[find(std::get<0>(ex->hkeys[t]))].push_back(t);
     const bool chain_tasks = std::getenv("GHX_NO_CHAIN") == nullptr;
+    const bool ring_mode = ex->ring;
     for (auto &kv : chains) {
       std::vector<int32_t> &ts = kv.second;
       std::sort(ts.begin(), ts.end());
       bool uniform = chain_tasks && ts.size() <= 32;
       for (int32_t t : ts) uniform = uniform && ex->htags[t].nvec == ex->htags[ts[0]].nvec;
+      if (uniform && ring_mode) {
+        std::vector<int32_t> order = ring_order(ex, ts);
+        if (!order.empty()) {
+          const DevTag &t0 = ex->htags[order[0]];
+          const int k = (int)order.size();
+          const int streams = 16 / k;
+          const uint32_t ncols = t0.nz * (t0.nvec / (t0.ny * t0.nz));
+          const int off = (int)ex->hchain.size();
+          ex->hchain.insert(ex->hchain.end(), order.begin(), order.end());
+          ex->nring += 2 * k;
+          for (uint32_t y0 = 0, seg = 0; y0 < t0.ny; y0 += kRingRows, ++seg)
+            for (uint32_t q = 0; q < ncols; q += streams)
+              swaps.push_back(make_int4(off, (int)q, -4, k | (int)(seg << 5)));
+          continue;
+        }
+      }
       if (uniform) {
         const int off = (int)ex->hchain.size();
         ex->hchain.insert(ex->hchain.end(), ts.begin(), ts.end());
@@ -906,6 +1047,23 @@ void ghx_exec_free(ghx_exec *ex) {
   delete ex;
 }
 
+int ghx_exec_set_ring(ghx_exec *ex, int32_t on) {
+  if (!ex) {
+    set_error("ghx_exec_set_ring: null handle");
+    return GHX_EINVAL;
+  }
+  std::lock_guard<std::mutex> lk(ex->mu);
+  if (ex->uploaded) {
+    set_error("ghx_exec_set_ring: the executor has already run");
+    return GHX_EINVAL;
+  }
+  if (ex->ring != (on != 0)) {
+    ex->ring = on != 0;
+    build_tasks(ex);
+  }
+  return GHX_OK;
+}
+
 int ghx_exec_set_grid(ghx_exec *ex, int32_t blocks, int32_t threads) {
   if (!ex || threads != kThreads || blocks < 0) {
     set_error("ghx_exec_set_grid: only 256-thread blocks are compiled");
@@ -1006,7 +1164,9 @@ int ghx_exec_run(ghx_exec *ex, void *const *ptrs, int64_t nptrs, void *stream) {
   if (const char *v = std::getenv("GHX_BATCH")) batch = std::max(1, std::atoi(v));
   int ld = ex->ld_mode;
   if (ld == 0 && !ex->nc_loads) ld = 2;  // sources may alias destinations (ParallelCopy): no .nc
-  switch (ld) {
+  if (ex->nring) {  // ring tasks present: the ring-capable instantiation
+    ghx_copy_kernel<2, true><<<ex->blocks, ex->threads, 0, st>>>(ex->dtags, ex->dtasks, ntasks, ex->dchain, ex->dcounter, batch);
+  } else switch (ld) {
     case 0: ghx_copy_kernel<0><<<ex->blocks, ex->threads, 0, st>>>(ex->dtags, ex->dtasks, ntasks, ex->dchain, ex->dcounter, batch); break;
     case 1: ghx_copy_kernel<1><<<ex->blocks, ex->threads, 0, st>>>(ex->dtags, ex->dtasks, ntasks, ex->dchain, ex->dcounter, batch); break;
     case 2: ghx_copy_kernel<2><<<ex->blocks, ex->threads, 0, st>>>(ex->dtags, ex->dtasks, ntasks, ex->dchain, ex->dcounter, batch); break;

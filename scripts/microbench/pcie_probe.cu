@@ -18,14 +18,17 @@
   } while (0)
 
 // LPS lanes cooperate on one access of BYTES bytes (each lane BYTES/LPS, 16 or 32 B)
+__device__ int64_t g_perm_mul = 1;  // 1: sequential seams; large odd: scattered order
+
 template <int BYTES, int LPS, bool WRITE, int PF = 0>
 __global__ void probe(char *buf, int64_t n, int64_t stride, unsigned *sink) {
+  const int64_t pm = g_perm_mul;
   constexpr int PER = BYTES / LPS;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
   uint32_t acc = 0;
   for (int64_t t = tid; t < n * LPS; t += nthr) {
-    const int64_t s = t / LPS;
+    const int64_t s = (int64_t)(((unsigned __int128)(t / LPS) * (uint64_t)pm) % (uint64_t)n);
     const int part = (int)(t % LPS);
     char *p = buf + s * stride + part * PER;
     if (WRITE) {
@@ -113,6 +116,14 @@ int main(int argc, char **argv) {
   run<128, 4, true>("write 128B (4 lanes x32)", d, n, stride, sink);
   run<256, 8, true>("write 256B (8 lanes x32)", d, n, stride, sink);
   run<512, 16, true>("write 512B (16 lanes x32)", d, n, stride, sink);
+  run<512, 16, false>("read 512B (16 lanes x32)", d, n, stride, sink);
+  int64_t pm = 1000003;  // coprime with n: a scattered permutation of the seams
+  cudaMemcpyToSymbol(g_perm_mul, &pm, sizeof(pm));
+  printf("scattered order (seam i -> i * %lld mod n)\n", (long long)pm);
+  run<32, 1, false>("read 32B", d, n, stride, sink);
+  run<64, 2, false>("read 64B (2 lanes x32)", d, n, stride, sink);
+  run<32, 1, true>("write 32B", d, n, stride, sink);
+  run<64, 2, true>("write 64B (2 lanes x32)", d, n, stride, sink);
   run<512, 16, false>("read 512B (16 lanes x32)", d, n, stride, sink);
   CK(cudaGetLastError());
   return 0;

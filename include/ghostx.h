@@ -177,6 +177,28 @@ int ghx_fill_hash(void *fab, const int64_t fab_box[6], int32_t ncomp, const int6
 int ghx_fill_hash_wrapped(void *fab, const int64_t fab_box[6], int32_t ncomp, const int64_t domain_box[6],
                           const int32_t periodic[3], uint64_t seed, int32_t elem_bytes, void *stream);
 
+/* ----------------------------------------------------------------- arena */
+
+/* Pooled arena (reference arena.py:87-197): slabs + LIFO free lists per
+ * (padded size, alignment); kind SYSTEM makes one allocation per request.
+ * memory: device HBM (device = CUDA ordinal), pinned+mapped host, or plain
+ * host memory (host-only tests).  Thread-safe.  A zero-byte allocation
+ * returns NULL; freeing a pointer that is not a live block (double free)
+ * returns GHX_EOVERLAP.  Stats: reserved, in-use (padded), alloc calls,
+ * slab growths. */
+#define GHX_ARENA_POOLED 0
+#define GHX_ARENA_SYSTEM 1
+#define GHX_ARENA_DEVICE 0
+#define GHX_ARENA_PINNED 1
+#define GHX_ARENA_HOST 2
+typedef struct ghx_arena ghx_arena;
+int ghx_arena_create(int32_t kind, int32_t memory, int32_t device, size_t capacity_bytes, ghx_arena **out);
+int ghx_arena_alloc(ghx_arena *a, size_t nbytes, size_t align, void **out);
+int ghx_arena_free(ghx_arena *a, void *ptr);
+int ghx_arena_block_size(const ghx_arena *a, const void *ptr, size_t *padded);
+int ghx_arena_stats(const ghx_arena *a, int64_t out[4]);
+void ghx_arena_destroy(ghx_arena *a);
+
 /* Number of fused-copy kernel launches issued by this process. */
 int64_t ghx_launch_count(void);
 

@@ -18,7 +18,7 @@ REPO = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIBDIR, "libghostx.so")
-SOURCES = ["ghx_plan.cpp", "ghx_exec.cu", "ghx_runtime.cu", "ghx_amr.cu"]
+SOURCES = ["ghx_plan.cpp", "ghx_exec.cu", "ghx_runtime.cu", "ghx_amr.cu", "ghx_arena.cpp"]
 HEADERS = ["ghx_internal.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -51,6 +51,12 @@ _SIGS = {
     "ghx_exec_detail": (C.c_int, [P, PI64]),
     "ghx_exec_set_grid": (C.c_int, [P, I32, I32]),
     "ghx_exec_set_ring": (C.c_int, [P, I32]),
+    "ghx_arena_create": (C.c_int, [I32, I32, I32, C.c_size_t, C.POINTER(P)]),
+    "ghx_arena_alloc": (C.c_int, [P, C.c_size_t, C.c_size_t, C.POINTER(P)]),
+    "ghx_arena_free": (C.c_int, [P, P]),
+    "ghx_arena_block_size": (C.c_int, [P, P, C.POINTER(C.c_size_t)]),
+    "ghx_arena_stats": (C.c_int, [P, PI64]),
+    "ghx_arena_destroy": (None, [P]),
     "ghx_device_alloc": (C.c_int, [I32, C.c_size_t, C.POINTER(P)]),
     "ghx_device_free": (C.c_int, [P]),
     "ghx_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(P)]),
@@ -80,6 +86,8 @@ _SIGS = {
 
 INTERP_PC, INTERP_LINEAR = 0, 1
 ADVANCE_TILES, ADVANCE_CELLS = 0, 1
+ARENA_POOLED, ARENA_SYSTEM = 0, 1
+ARENA_DEVICE, ARENA_PINNED, ARENA_HOST = 0, 1, 2
 JOB_WORDS = 20  # int64 words per ghx_interp_job / ghx_avgdown_job
 
 EXPORTED = tuple(_SIGS)

@@ -59,6 +59,16 @@ def _torch_dtype(dt: np.dtype):
     return torch.float64 if np.dtype(dt).itemsize == 8 else torch.float32
 
 
+def _native_arena(arena):
+    """An arena from paper_2403_12179_b200.arena (pooled storage), or None:
+    anything else passed as ``arena=`` (the reference's CPU arenas) keeps the
+    one-allocation-per-MultiFab default."""
+    from . import arena as _arena_mod
+    if isinstance(arena, (_arena_mod.Arena, _arena_mod.AsyncArena)):
+        return arena
+    return None
+
+
 def _current_device() -> int:
     from . import comm
     return comm.current_ctx().device
@@ -67,15 +77,24 @@ def _current_device() -> int:
 class Slab:
     """One native allocation (device HBM or pinned host), freed on GC."""
 
-    def __init__(self, nbytes: int, device: int, memory: str = "device"):
+    def __init__(self, nbytes: int, device: int, memory: str = "device", arena=None):
         if memory not in ("device", "pinned"):
             raise ValueError(f"memory must be 'device' or 'pinned', got {memory!r}")
-        p = C.c_void_p()
-        if memory == "device":
-            N.check(N.lib.ghx_device_alloc(int(device), -(-int(nbytes) // 256) * 256, C.byref(p)))
+        self._block = None
+        if arena is not None:  # pooled storage (arena.py); 256-B aligned blocks
+            if getattr(arena, "memory", None) != memory:
+                raise ValueError(f"arena holds {getattr(arena, 'memory', '?')} memory, the MultiFab needs {memory}")
+            if memory == "device" and arena.device != int(device):
+                raise ValueError(f"arena is on device {arena.device}, the MultiFab on device {device}")
+            self._block = arena.alloc(-(-int(nbytes) // 256) * 256, 256)
+            self.ptr = self._block.address
         else:
-            N.check(N.lib.ghx_host_alloc(-(-int(nbytes) // 256) * 256, C.byref(p)))
-        self.ptr = int(p.value)
+            p = C.c_void_p()
+            if memory == "device":
+                N.check(N.lib.ghx_device_alloc(int(device), -(-int(nbytes) // 256) * 256, C.byref(p)))
+            else:
+                N.check(N.lib.ghx_host_alloc(-(-int(nbytes) // 256) * 256, C.byref(p)))
+            self.ptr = int(p.value)
         self.nbytes = int(nbytes)
         self.device = int(device)
         self.memory = memory
@@ -102,7 +121,11 @@ class Slab:
 
     def __del__(self):
         try:
-            if self.ptr:
+            if self._block is not None:
+                self._block.free()
+                self._block = None
+                self.ptr = 0
+            elif self.ptr:
                 (N.lib.ghx_device_free if self.memory == "device" else N.lib.ghx_host_free)(C.c_void_p(self.ptr))
                 self.ptr = 0
         except Exception:
@@ -125,7 +148,7 @@ class Fab:
         count = math.prod(shape)
         if _slab is None:
             dev = _current_device() if device is None else int(device)
-            _slab = Slab(count * self.dtype.itemsize, dev, memory)
+            _slab = Slab(count * self.dtype.itemsize, dev, memory, arena=_native_arena(arena))
             _offset = 0
             if config.debug:
                 N.check(N.lib.ghx_memset_u64(C.c_void_p(_slab.ptr), config.POISON_BITS64 if self.dtype.itemsize == 8
@@ -361,6 +384,7 @@ class MultiFab:
         if any(g < 0 for g in self.ngrow):
             raise ValueError("ngrow components must be >= 0")
         self.geom = geom
+        self.arena = arena
         self.dtype = config.real_dtype
         ctx = comm.current_ctx()
         self.rank = ctx.rank if rank is None else int(rank)
@@ -389,7 +413,7 @@ class MultiFab:
         if not self.local_indices:
             self._ptrs = np.zeros(0, np.uint64)
             return
-        self._slab = Slab(total, self.device, self.memory)
+        self._slab = Slab(total, self.device, self.memory, arena=_native_arena(self.arena))
         if config.debug:
             N.check(N.lib.ghx_memset_u64(C.c_void_p(self._slab.ptr), config.POISON_BITS64 if item == 8
                                          else (config.POISON_BITS32 << 32) | config.POISON_BITS32,

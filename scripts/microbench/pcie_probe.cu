@@ -7,6 +7,8 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
+#include <sys/mman.h>
 
 #define CK(x)                                                                             \
   do {                                                                                    \
@@ -86,15 +88,24 @@ void run(const char *name, char *buf, int64_t n, int64_t stride, unsigned *sink)
 int main(int argc, char **argv) {
   const int64_t stride = 544;
   const bool wc = argc > 1 && argv[1][0] == 'w';
+  const bool huge = argc > 1 && argv[1][0] == 'h';
   const int64_t bytes = 1ll << 30;
   const int64_t n = bytes / stride - 1;
   char *h, *d;
   unsigned *sink;
-  CK(cudaHostAlloc(&h, bytes, cudaHostAllocMapped | (wc ? cudaHostAllocWriteCombined : 0)));
+  if (huge) {  // 2 MiB-aligned anonymous memory with transparent huge pages, then registered
+    h = (char *)mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (h == MAP_FAILED) { printf("mmap failed\n"); return 1; }
+    printf("madvise(MADV_HUGEPAGE) rc=%d\n", madvise(h, bytes, MADV_HUGEPAGE));
+    for (int64_t i = 0; i < bytes; i += 4096) h[i] = 1;
+    CK(cudaHostRegister(h, bytes, cudaHostRegisterMapped));
+  } else {
+    CK(cudaHostAlloc(&h, bytes, cudaHostAllocMapped | (wc ? cudaHostAllocWriteCombined : 0)));
+  }
   CK(cudaHostGetDevicePointer((void **)&d, h, 0));
   CK(cudaMalloc(&sink, 4));
   for (int64_t i = 0; i < bytes; i += 4096) h[i] = 1;
-  printf("%s pinned mapped host, stride", wc ? "write-combined" : "cached");
+  printf("%s pinned mapped host, stride", wc ? "write-combined" : huge ? "THP-registered" : "cached");
   printf(" %lld, %lld accesses\n", (long long)stride, (long long)n);
   run<16, 1, false>("read 16B", d, n, stride, sink);
   run<32, 1, false>("read 32B", d, n, stride, sink);

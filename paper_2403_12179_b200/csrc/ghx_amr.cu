@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(kAmrThreads, 3) interp_kernel(const DevInterpJ
 
 // One thread per coarse cell: acc = child(0,0,0), then += children in
 // (oz, oy, ox) loop order, then acc / ratio^D (amr.py:254-264).
-template <class T>
+template <class T, bool R222>
 __global__ void __launch_bounds__(kAmrThreads, 4) avgdown_kernel(const DevAvgJob *__restrict__ jobs,
                                                               const int4 *__restrict__ btasks, int ncomp, int r0,
                                                               int r1, int r2, T rpow) {
@@ -141,6 +141,19 @@ __global__ void __launch_bounds__(kAmrThreads, 4) avgdown_kernel(const DevAvgJob
                        (cidx[2] - J.c.lo[2]) * J.c.n[0] * J.c.n[1];
     const T *fine = reinterpret_cast<const T *>(J.fine);
     T *crse = reinterpret_cast<T *>(J.crse);
+    if (R222) {  // ratio 2 in 3-D: all eight children loaded before the ordered sum
+      for (int c = 0; c < ncomp; ++c) {
+        const T *f = fine + fo + c * fsc;
+        T v[8];
+#pragma unroll
+        for (int o = 0; o < 8; ++o) v[o] = __ldg(f + (o & 1) + ((o >> 1) & 1) * fsy + (o >> 2) * fsz);
+        T acc = v[0];
+#pragma unroll
+        for (int o = 1; o < 8; ++o) acc = add_rn(acc, v[o]);  // (oz, oy, ox) order, ox fastest
+        crse[co + c * csc] = div_rn(acc, rpow);
+      }
+      continue;
+    }
     for (int c = 0; c < ncomp; ++c) {
       const T *f = fine + fo + c * fsc;
       T acc = T(0);
@@ -180,9 +193,11 @@ __global__ void __launch_bounds__(kAmrThreads, 4) advance_kernel(const DevAvgJob
   T *o = reinterpret_cast<T *>(J.crse) + (x - J.c.lo[0]) + (y - J.c.lo[1]) * osy + (z - J.c.lo[2]) * osz;
   T um = DIM >= 3 ? __ldg(u - usz) : T(0);
   T uc = __ldg(u);
+  T up = DIM >= 3 ? __ldg(u + usz) : T(0);
 #pragma unroll 4
   for (int k = 0; k < bt.w; ++k) {
-    const T up = DIM >= 3 ? __ldg(u + usz) : T(0);
+    // the plane after next is requested a step early (more DRAM loads in flight)
+    const T upp = (DIM >= 3 && k + 1 < bt.w) ? __ldg(u + 2 * usz) : T(0);
     const T two_u = mul_rn(T(2), uc);
     T acc = uc;
     acc = add_rn(acc, mul_rn(c0, add_rn(sub_rn(__ldg(u + 1), two_u), __ldg(u - 1))));
@@ -191,6 +206,7 @@ __global__ void __launch_bounds__(kAmrThreads, 4) advance_kernel(const DevAvgJob
     *o = acc;
     um = uc;
     uc = up;
+    up = upp;
     u += usz;
     o += osz;
   }
@@ -360,12 +376,13 @@ int xfer_launch(const ghx_xfer *x, cudaStream_t st) {
 #undef GHX_ADV
   } else {
     const DevAvgJob *p = static_cast<const DevAvgJob *>(x->djobs);
+    const bool r222 = x->r[0] == 2 && x->r[1] == 2 && x->r[2] == 2;
     if (x->elem_bytes == 8)
-      avgdown_kernel<double><<<x->blocks, kAmrThreads, 0, st>>>(p, x->dtasks, x->ncomp, x->r[0], x->r[1], x->r[2],
-                                                                (double)x->rpow);
+      (r222 ? avgdown_kernel<double, true> : avgdown_kernel<double, false>)<<<x->blocks, kAmrThreads, 0, st>>>(
+          p, x->dtasks, x->ncomp, x->r[0], x->r[1], x->r[2], (double)x->rpow);
     else
-      avgdown_kernel<float><<<x->blocks, kAmrThreads, 0, st>>>(p, x->dtasks, x->ncomp, x->r[0], x->r[1], x->r[2],
-                                                               (float)x->rpow);
+      (r222 ? avgdown_kernel<float, true> : avgdown_kernel<float, false>)<<<x->blocks, kAmrThreads, 0, st>>>(
+          p, x->dtasks, x->ncomp, x->r[0], x->r[1], x->r[2], (float)x->rpow);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "ghx_xfer_run: launch");

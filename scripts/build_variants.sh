@@ -8,7 +8,7 @@ C=paper_2403_12179_b200/csrc
 for spec in "$@"; do
   tag=${spec%%:*}; flags=${spec#*:}
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -shared -Xcompiler -fPIC \
-    -I include -I $C -cudart static $flags -o build/variants/$tag.so $C/ghx_plan.cpp $C/ghx_exec.cu $C/ghx_runtime.cu &
+    -I include -I $C -cudart static $flags -o build/variants/$tag.so $C/*.cpp $C/*.cu &
 done
 wait
 ls build/variants

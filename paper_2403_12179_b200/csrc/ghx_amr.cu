@@ -105,12 +105,18 @@ __global__ void __launch_bounds__(kAmrThreads, 3) interp_kernel(const DevInterpJ
     const int64_t step[3] = {1, csy, csz};
     for (int c = 0; c < ncomp; ++c) {
       const T *cc = crse + co + c * csc;
-      T v = __ldg(cc);
+      // every coarse value this cell needs is requested before the arithmetic
+      T v = __ldg(cc), up[3], dn[3];
       if (LINEAR) {
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
+          up[d] = d < spacedim ? __ldg(cc + step[d]) : T(0);
+          dn[d] = d < spacedim ? __ldg(cc - step[d]) : T(0);
+        }
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
           if (d >= spacedim) break;
-          const T slope = mul_rn(T(0.5), sub_rn(__ldg(cc + step[d]), __ldg(cc - step[d])));
+          const T slope = mul_rn(T(0.5), sub_rn(up[d], dn[d]));
           v = T(__dadd_rn((double)v, __dmul_rn((double)slope, off[d])));
         }
       }

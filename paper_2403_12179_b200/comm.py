@@ -416,12 +416,12 @@ class CommPlan:
         host = getattr(dst_mf, "memory", "device") == "pinned" or getattr(src_mf, "memory", "device") == "pinned"
         ring = {"1": True, "0": False}.get(os.environ.get("GHX_RING", ""), host)
         key = (rank, kind, src_mf.ngrow.comps, src_mf.ncomp, dst_mf.ngrow.comps, dst_mf.ncomp,
-               scomp, dcomp, ncomp, dst_mf.dtype.itemsize, dst_mf.device, ring)
+               scomp, dcomp, ncomp, dst_mf.dtype.itemsize, dst_mf.device, ring, host)
         with self._lock:
             ex = self._execs.get(key)
             if ex is None:
                 ex = Executor(self, rank, kind, src_mf.storage_rows(), src_mf.ncomp, dst_mf.storage_rows(),
-                              dst_mf.ncomp, scomp, dcomp, ncomp, dst_mf.dtype.itemsize, dst_mf.device, ring)
+                              dst_mf.ncomp, scomp, dcomp, ncomp, dst_mf.dtype.itemsize, dst_mf.device, ring, host)
                 self._execs[key] = ex
         return ex
 
@@ -440,13 +440,18 @@ class Executor:
     tag table; ``run`` is one launch of the fused copy kernel)."""
 
     def __init__(self, plan, rank, kind, src_rows, src_nc, dst_rows, dst_nc, scomp, dcomp, ncomp, item, device,
-                 ring=False):
+                 ring=False, host=False):
         h = C.c_void_p()
         N.check(N.lib.ghx_exec_create(plan._h, rank, kind, N.i64p(src_rows), src_nc, N.i64p(dst_rows), dst_nc,
                                       scomp, dcomp, ncomp, item, device, C.byref(h)))
         self._h = h
         if ring:
             N.check(N.lib.ghx_exec_set_ring(h, 1))
+        if host:
+            # fabs in host memory: the PCIe / IOMMU path saturates with few
+            # concurrent warps and degrades with many (scattered 32-64 B
+            # requests); 8 CTAs measured best (C2 e2e 9.6 -> 7.4 ms, DESIGN.md)
+            N.check(N.lib.ghx_exec_set_grid(h, int(os.environ.get("GHX_HOST_BLOCKS", "8")), 256))
         self.plan = plan
         self.nsrc = len(src_rows)
         self.ndst = len(dst_rows)

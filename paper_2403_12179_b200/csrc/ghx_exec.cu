@@ -778,8 +778,11 @@ void build_tasks(ghx_exec *ex) {
           const int off = (int)ex->hchain.size();
           ex->hchain.insert(ex->hchain.end(), order.begin(), order.end());
           ex->nring += 2 * k;
-          for (uint32_t y0 = 0, seg = 0; y0 < t0.ny; y0 += kRingRows, ++seg)
-            for (uint32_t q = 0; q < ncols; q += streams)
+          // column-major (q, then row segment): concurrent warps stay on few
+          // host pages (fabs in host memory are the ring's use)
+          const uint32_t nseg = (t0.ny + kRingRows - 1) / kRingRows;
+          for (uint32_t q = 0; q < ncols; q += streams)
+            for (uint32_t seg = 0; seg < nseg; ++seg)
               swaps.push_back(make_int4(off, (int)q, -4, k | (int)(seg << 5)));
           continue;
         }

@@ -174,7 +174,11 @@ def average_down(fine: MultiFab, coarse: MultiFab, ratio: int, backend=None) -> 
                                                fine.device, C.byref(h)))
         xf = fine._peer_cache[key] = _Xfer(h.value, fine.device)
     xf.run()
-    comm.parallel_copy(coarse, tmp, backend=backend)
+    if comm.current_ctx().nranks == 1:  # stream-ordered: one host wait
+        comm.prepare_parallel_copy(coarse, tmp).enqueue(_stream(fine.device))
+        _sync(fine.device)
+    else:
+        comm.parallel_copy(coarse, tmp, backend=backend)
 
 
 # ---------------------------------------------------------------- fill_patch
@@ -241,8 +245,14 @@ def fill_patch(fine: MultiFab, coarse: MultiFab, fine_geom: Geometry, coarse_geo
 
     FillBoundary (fused exchange) -> gather of the coarse cells under each
     fine fab's uncovered ghost regions (fused exchange, plan-cached target
-    slab) -> one interp launch over every (fab, region) job."""
-    comm.fill_boundary(fine, fine_geom, backend=backend)
+    slab) -> one interp launch over every (fab, region) job.  With a single
+    rank the three steps are enqueued back to back on the current stream and
+    the host waits once at the end."""
+    serial = comm.current_ctx().nranks == 1
+    if serial:
+        comm.prepare_fill_boundary(fine, fine_geom).enqueue(_stream(fine.device))
+    else:
+        comm.fill_boundary(fine, fine_geom, backend=backend)
     reach = 1 if scheme == LINEAR else 0
     key = comm.PlanKey(coarse.ba.uid, coarse.dm.uid, fine.ba.uid, fine.dm.uid, (reach,) * len(fine.ngrow),
                        fine.ngrow.comps, fine.ba.ixtype.flags, fine_geom.periodic, "fill_patch")
@@ -260,9 +270,16 @@ def fill_patch(fine: MultiFab, coarse: MultiFab, fine_geom: Geometry, coarse_geo
         fine.plan_builds += 1
     targets, gather_list, dst_ranks, plan = cached
     if not targets:
+        if serial:
+            _sync(fine.device)
         return
     owned = comm.gather_targets(plan, gather_list, dst_ranks, coarse)
-    comm.gather_fabs(gather_list, dst_ranks, owned, coarse, coarse_geom, backend=backend, plan=plan)
+    if serial:
+        if not plan.is_empty:
+            comm.exchange_for(plan, coarse, comm._gather_set(plan, gather_list, dst_ranks, coarse), 0, 0,
+                              coarse.ncomp).enqueue(_stream(fine.device))
+    else:
+        comm.gather_fabs(gather_list, dst_ranks, owned, coarse, coarse_geom, backend=backend, plan=plan)
     xkey = ("fill_patch_interp", key, int(ratio), scheme, fine.ncomp)
     xf = fine._peer_cache.get(xkey)
     if xf is None:

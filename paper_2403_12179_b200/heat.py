@@ -132,7 +132,10 @@ def heat_step(levels: list, geoms: list, dt: float, diffusivity: float, ref_rati
                 _stencil(u, w, dt, diffusivity, geoms[lv], "interior").run()
         done = torch.cuda.Event()
         done.record(side)
-    comm.fill_boundary(levels[0][0], geoms[0], backend=backend)
+    if comm.current_ctx().nranks == 1:  # stream-ordered, no host wait before the stencil
+        comm.prepare_fill_boundary(levels[0][0], geoms[0]).enqueue(main.cuda_stream)
+    else:
+        comm.fill_boundary(levels[0][0], geoms[0], backend=backend)
     if len(levels) > 1:
         fill_patch(levels[1][0], levels[0][0], geoms[1], geoms[0], ref_ratio, LINEAR, backend=backend)
     for lv, (u, w) in enumerate(levels):

@@ -27,7 +27,7 @@ done
 timeout 600 python bench.py --impl reference --steps 20 --warmup 3 > gpurun_out/prof/bench_ref_C2.json 2> gpurun_out/prof/bench_ref_C2.log
 echo "bench ref rc=$?"
 # level transfers
-for op in fill_patch average_down; do
+for op in fill_patch average_down heat; do
   timeout 600 python bench_amr.py --op $op > gpurun_out/prof/bench_amr_$op.json 2> gpurun_out/prof/bench_amr_$op.log
   echo "bench_amr $op rc=$?"
 done
@@ -37,6 +37,9 @@ timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,launch__registers_per_thread,sm__warps_active.avg.pct_of_peak_sustained_active \
   --clock-control none --csv -k regex:"avgdown_kernel" -c 2 python bench_amr.py --op average_down --steps 3 --warmup 3 \
   > gpurun_out/prof/traffic_avgdown.csv 2> gpurun_out/prof/traffic_avgdown.err
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,launch__registers_per_thread,sm__warps_active.avg.pct_of_peak_sustained_active \
+  --clock-control none --csv -k regex:"advance_kernel" -c 2 python bench_amr.py --op heat --steps 3 --warmup 3 \
+  > gpurun_out/prof/traffic_advance.csv 2> gpurun_out/prof/traffic_advance.err
 echo "amr ncu done"
 # microbenchmarks behind the roofline discussion
 (cd scripts/microbench && nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/seam_probe seam_probe.cu \

@@ -31,6 +31,13 @@ for c in ["C1", "C2", "C3", "C4", "C5"]:
     shutil.copy(f"{src}/bench_{c}.json", f"profiles/{tag}_bench_{c}.json")
 json.dump(traffic, open("profiles/ncu_traffic.json", "w"), indent=1)
 for f in os.listdir(src):
+    if f.startswith("bench_amr_") and f.endswith(".json"):
+        shutil.copy(f"{src}/{f}", f"profiles/{tag}_{f}")
+    if f in ("traffic_interp.csv", "traffic_avgdown.csv", "traffic_advance.csv"):
+        name = {"traffic_interp.csv": "interp", "traffic_avgdown.csv": "avgdown", "traffic_advance.csv": "advance"}[f]
+        shutil.copy(f"{src}/{f}", f"profiles/{tag}_ncu_{name}_kernel.csv")
+    if (f.startswith("seam_probe_") or f.startswith("pcie_probe")) and f.endswith(".txt"):
+        shutil.copy(f"{src}/{f}", f"profiles/{tag}_{f}")
     if f.startswith("launches_") and f.endswith(".csv"):
         shutil.copy(f"{src}/{f}", f"profiles/{tag}_{f}")
     if f.startswith("bench_ref_") and f.endswith(".json"):

@@ -432,7 +432,7 @@ def run_ours(args, cfg, rank, world):
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": round(mean_ms_max, 5), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "scaling": "weak" if cfg.get("weak") else "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (splitmix64 counter-hash valid cells, sNaN-poisoned ghosts)",
         "config": {"workload": cfg["desc"], "domain": list(cfg["ext"]), "box": cfg["box"], "ncomp": cfg["ncomp"],
                    "nghost": cfg["ngrow"], "boxes": len(L["ba"]), "segments": plan.num_segments,

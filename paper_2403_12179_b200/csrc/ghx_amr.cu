@@ -158,8 +158,7 @@ __global__ void __launch_bounds__(kAmrThreads, 4) avgdown_kernel(const DevAvgJob
         for (int o = 1; o < 8; ++o) acc = add_rn(acc, v[o]);  // (oz, oy, ox) order, ox fastest
         crse[co + c * csc] = div_rn(acc, rpow);
       }
-      continue;
-    }
+    } else {
     for (int c = 0; c < ncomp; ++c) {
       const T *f = fine + fo + c * fsc;
       T acc = T(0);
@@ -173,6 +172,7 @@ __global__ void __launch_bounds__(kAmrThreads, 4) avgdown_kernel(const DevAvgJob
           }
       crse[co + c * csc] = div_rn(acc, rpow);
     }
+    }
   }
 }
 
@@ -182,7 +182,13 @@ __global__ void __launch_bounds__(kAmrThreads, 4) avgdown_kernel(const DevAvgJob
 // 2.5-D blocking: a block is a 32 x 8 (x, y) tile of one job that marches
 // kAdvZ planes in z, carrying u[z-1], u[z], u[z+1] in registers, so each
 // source value comes from HBM once (x/y neighbours hit L1).
-constexpr int kAdvTX = 32, kAdvTY = 8, kAdvZ = 16;
+#ifndef GHX_ADV_PF
+#define GHX_ADV_PF 2
+#endif
+#ifndef GHX_ADV_Z
+#define GHX_ADV_Z 16
+#endif
+constexpr int kAdvTX = 32, kAdvTY = 8, kAdvZ = GHX_ADV_Z, kAdvPF = GHX_ADV_PF;
 
 template <class T, int DIM>
 __global__ void __launch_bounds__(kAmrThreads, 4) advance_kernel(const DevAvgJob *__restrict__ jobs,
@@ -197,13 +203,19 @@ __global__ void __launch_bounds__(kAmrThreads, 4) advance_kernel(const DevAvgJob
   const int64_t osy = J.c.n[0], osz = J.c.n[0] * J.c.n[1];
   const T *u = reinterpret_cast<const T *>(J.fine) + (x - J.f.lo[0]) + (y - J.f.lo[1]) * usy + (z - J.f.lo[2]) * usz;
   T *o = reinterpret_cast<T *>(J.crse) + (x - J.c.lo[0]) + (y - J.c.lo[1]) * osy + (z - J.c.lo[2]) * osz;
+  // register queue of the next kAdvPF planes: plane z+kAdvPF is requested
+  // kAdvPF - 1 steps before it is used (more DRAM loads in flight per thread)
   T um = DIM >= 3 ? __ldg(u - usz) : T(0);
   T uc = __ldg(u);
-  T up = DIM >= 3 ? __ldg(u + usz) : T(0);
+  T q[kAdvPF];
+#pragma unroll
+  for (int a = 0; a < kAdvPF; ++a) q[a] = (DIM >= 3 && a < bt.w) ? __ldg(u + (a + 1) * usz) : T(0);
 #pragma unroll 4
   for (int k = 0; k < bt.w; ++k) {
-    // the plane after next is requested a step early (more DRAM loads in flight)
-    const T upp = (DIM >= 3 && k + 1 < bt.w) ? __ldg(u + 2 * usz) : T(0);
+    const T up = q[0];
+#pragma unroll
+    for (int a = 0; a + 1 < kAdvPF; ++a) q[a] = q[a + 1];
+    q[kAdvPF - 1] = (DIM >= 3 && k + kAdvPF < bt.w) ? __ldg(u + (kAdvPF + 1) * usz) : T(0);
     const T two_u = mul_rn(T(2), uc);
     T acc = uc;
     acc = add_rn(acc, mul_rn(c0, add_rn(sub_rn(__ldg(u + 1), two_u), __ldg(u - 1))));
@@ -212,7 +224,6 @@ __global__ void __launch_bounds__(kAmrThreads, 4) advance_kernel(const DevAvgJob
     *o = acc;
     um = uc;
     uc = up;
-    up = upp;
     u += usz;
     o += osz;
   }

@@ -840,9 +840,12 @@ void build_tasks(ghx_exec *ex) {
     // small fabs: sweep the destination fabs in order, so the tasks that
     // share a fab's lines (seam sectors, face rows) run close in time and
     // hit in L2 (C4: -23 % time, C2: -6 %; measured)
-    auto key = [&](const int4 &t) -> std::pair<int64_t, int64_t> {
+    // key: (destination fab, component, position in the component)
+    auto key = [&](const int4 &t) -> std::tuple<int64_t, int64_t, int64_t> {
       const int32_t tag = (t.z == -4 || t.z == -3) ? ex->hchain[t.x] : t.x;
-      return {std::get<1>(ex->hkeys[tag]), (int64_t)t.y};
+      const DevTag &d = ex->htags[tag];
+      const int64_t per_comp = std::max<int64_t>(1, (int64_t)d.nxv * d.ny * d.nz);
+      return {std::get<1>(ex->hkeys[tag]), (int64_t)t.y / per_comp, (int64_t)t.y % per_comp};
     };
     std::stable_sort(a.begin(), a.end(), [&](const int4 &l, const int4 &r) { return key(l) < key(r); });
   }

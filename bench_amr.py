@@ -157,6 +157,10 @@ def heat_bench(args, amr, cdom, cgeom, cba, flush, clean, hbm, peak_src):
             state["levels"] = H.heat_step(state["levels"], [cgeom], dt, kappa, overlap=ov)
         t_mean, _ = timed(step, args.steps, args.warmup, flush, clean)
         res["overlap" if ov else "serial"] = round(t_mean * 1e3, 4)
+    loop = H.HeatLoop(state["levels"], [cgeom], dt, kappa)
+    t_graph, _ = timed(loop.step, args.steps, args.warmup, flush, clean)
+    res["graph"] = round(t_graph * 1e3, 4)
+    state["levels"] = loop.levels
     cells = sum(b.num_pts for b in cba)
     xf = H._stencil(state["levels"][0][0], state["levels"][0][1], dt, kappa, cgeom, "all")
     k_mean, _ = timed(xf.run, args.steps, args.warmup, flush, clean)
@@ -164,6 +168,7 @@ def heat_bench(args, amr, cdom, cgeom, cba, flush, clean, hbm, peak_src):
     return {"metric": "heat_step cells/s (FillBoundary + 7-point stencil, reference demo loop body)",
             "value": round(cells / (res["serial"] * 1e-3) / 1e9, 3), "unit": "Gcell/s",
             "ms_per_step": res["serial"], "ms_per_step_overlap": res["overlap"],
+            "ms_per_step_cuda_graph": res["graph"],
             "config": {"workload": f"{N_CRSE}^3 periodic, {BOX}^3 boxes, ncomp 1, nghost 1, float64 "
                                    "(the reference heat demo layout)",
                        "l2": "flushed before every step (512 MiB write + 256 MiB clean read, outside the events)"},

@@ -144,7 +144,7 @@ def _restriction_layout(fine: MultiFab, ratio: int) -> MultiFab:
     return tmp
 
 
-def average_down(fine: MultiFab, coarse: MultiFab, ratio: int, backend=None) -> None:
+def average_down(fine: MultiFab, coarse: MultiFab, ratio: int, backend=None, *, _wait: bool = True) -> None:
     """Covered coarse cells become the mean of their ratio^D fine children
     (amr.py:235-266): one restriction launch over the local fine fabs, then
     ParallelCopy into ``coarse``."""
@@ -176,7 +176,8 @@ def average_down(fine: MultiFab, coarse: MultiFab, ratio: int, backend=None) -> 
     xf.run()
     if comm.current_ctx().nranks == 1:  # stream-ordered: one host wait
         comm.prepare_parallel_copy(coarse, tmp).enqueue(_stream(fine.device))
-        _sync(fine.device)
+        if _wait:
+            _sync(fine.device)
     else:
         comm.parallel_copy(coarse, tmp, backend=backend)
 
@@ -239,7 +240,7 @@ def _coarse_fill_targets(fine_ba: BoxArray, ngrow: IntVect, geom: Geometry) -> d
 
 
 def fill_patch(fine: MultiFab, coarse: MultiFab, fine_geom: Geometry, coarse_geom: Geometry, ratio: int,
-               scheme: str = LINEAR, backend=None) -> None:
+               scheme: str = LINEAR, backend=None, *, _wait: bool = True) -> None:
     """Fill fine ghost cells: same-level data where available, interpolated
     coarse data elsewhere; valid cells are never modified (amr.py:355-397).
 
@@ -270,7 +271,7 @@ def fill_patch(fine: MultiFab, coarse: MultiFab, fine_geom: Geometry, coarse_geo
         fine.plan_builds += 1
     targets, gather_list, dst_ranks, plan = cached
     if not targets:
-        if serial:
+        if serial and _wait:
             _sync(fine.device)
         return
     owned = comm.gather_targets(plan, gather_list, dst_ranks, coarse)
@@ -299,4 +300,5 @@ def fill_patch(fine: MultiFab, coarse: MultiFab, fine_geom: Geometry, coarse_geo
         xf = fine._peer_cache[xkey] = _prepare_interp(jobs, fine.ncomp, int(ratio), scheme, fine.dtype.itemsize,
                                                       fine.device)
     xf.run()
-    _sync(fine.device)
+    if _wait or not serial:
+        _sync(fine.device)

@@ -562,7 +562,18 @@ struct ghx_exec {
   DevTag *dtags = nullptr;
   int4 *dtasks = nullptr;
   void **dptrs = nullptr;
-  std::vector<void *> cached_ptrs;
+  // bound descriptor tables, one per pointer table in use (e.g. the u and
+  // unew MultiFabs of a time loop share this executor): switching tables
+  // costs nothing after the first bind, and CUDA-graph replays never
+  // re-upload (binding 0 is dtags / dptrs above)
+  struct Binding {
+    std::vector<void *> ptrs;
+    DevTag *dtags;
+    void **dptrs;
+    uint64_t last_use;
+  };
+  std::vector<Binding> bindings;
+  uint64_t uses = 0;
   int64_t nptrs = 0;
   int blocks = 0, threads = kThreads;
   bool uploaded = false;
@@ -1067,6 +1078,10 @@ extern "C" {
 void ghx_exec_free(ghx_exec *ex) {
   if (!ex) return;
   DeviceGuard g(ex->device);
+  for (size_t i = 1; i < ex->bindings.size(); ++i) {
+    cudaFree(ex->bindings[i].dtags);
+    cudaFree(ex->bindings[i].dptrs);
+  }
   if (ex->dtags) cudaFree(ex->dtags);
   if (ex->dtasks) cudaFree(ex->dtasks);
   if (ex->dchain) cudaFree(ex->dchain);
@@ -1148,8 +1163,10 @@ int ghx_exec_run(ghx_exec *ex, void *const *ptrs, int64_t nptrs, void *stream) {
   DeviceGuard g(ex->device);
   if (int rc = exec_upload(ex)) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (ex->cached_ptrs.size() != (size_t)nptrs ||
-      std::memcmp(ex->cached_ptrs.data(), ptrs, nptrs * sizeof(void *)) != 0) {
+  ghx_exec::Binding *bd = nullptr;
+  for (auto &b : ex->bindings)
+    if (b.ptrs.size() == (size_t)nptrs && std::memcmp(b.ptrs.data(), ptrs, nptrs * sizeof(void *)) == 0) bd = &b;
+  if (!bd) {
     const uintptr_t amask = ex->nswap ? 31 : 15;
     for (int64_t i = 0; i < nptrs; ++i)
       if (reinterpret_cast<uintptr_t>(ptrs[i]) & amask) {
@@ -1170,20 +1187,44 @@ int ghx_exec_run(ghx_exec *ex, void *const *ptrs, int64_t nptrs, void *stream) {
           set_error("ghx_exec_run: FillBoundary executor needs src slot == dst slot for every fab");
           return GHX_EINVAL;
         }
-    ex->cached_ptrs.assign(ptrs, ptrs + nptrs);
+    constexpr size_t kMaxBindings = 4;
+    cudaError_t e = cudaSuccess;
+    if (ex->bindings.empty()) {
+      ex->bindings.push_back({{}, ex->dtags, ex->dptrs, 0});
+    } else if (ex->bindings.size() < kMaxBindings) {
+      ghx_exec::Binding nb{{}, nullptr, nullptr, 0};
+      e = cudaMalloc(&nb.dtags, std::max<size_t>(1, ex->htags.size()) * sizeof(DevTag));
+      if (e == cudaSuccess) e = cudaMalloc(&nb.dptrs, std::max<int64_t>(ex->nptrs, 1) * sizeof(void *));
+      if (e == cudaSuccess && !ex->htags.empty())
+        e = cudaMemcpyAsync(nb.dtags, ex->dtags, ex->htags.size() * sizeof(DevTag), cudaMemcpyDeviceToDevice, st);
+      if (e != cudaSuccess) {
+        if (nb.dtags) cudaFree(nb.dtags);
+        if (nb.dptrs) cudaFree(nb.dptrs);
+        return cuda_fail(e, "ghx_exec_run: binding");
+      }
+      ex->bindings.push_back(nb);
+    } else {  // reuse the least recently used binding (stream-ordered rebind)
+      size_t lru = 0;
+      for (size_t i = 1; i < ex->bindings.size(); ++i)
+        if (ex->bindings[i].last_use < ex->bindings[lru].last_use) lru = i;
+      std::swap(ex->bindings[lru], ex->bindings.back());
+    }
+    bd = &ex->bindings.back();
+    bd->ptrs.assign(ptrs, ptrs + nptrs);
     // pageable source: the copy has consumed the host table when this returns
-    cudaError_t e = cudaMemcpyAsync(ex->dptrs, ex->cached_ptrs.data(), nptrs * sizeof(void *),
-                                    cudaMemcpyHostToDevice, st);
+    e = cudaMemcpyAsync(bd->dptrs, bd->ptrs.data(), nptrs * sizeof(void *), cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess) {
       const int n = (int)ex->htags.size();
-      ghx_bind_kernel<<<std::min(1184, (n + 255) / 256), 256, 0, st>>>(ex->dtags, n, ex->dptrs);
+      ghx_bind_kernel<<<std::min(1184, (n + 255) / 256), 256, 0, st>>>(bd->dtags, n, bd->dptrs);
       e = cudaGetLastError();
     }
     if (e != cudaSuccess) {
-      ex->cached_ptrs.clear();
+      bd->ptrs.clear();
       return cuda_fail(e, "ghx_exec_run: pointer bind");
     }
   }
+  bd->last_use = ++ex->uses;
+  DevTag *const dtags = bd->dtags;
   const int ntasks = (int)ex->htasks.size();
   // tasks per atomic grab: single tasks balance the latency-bound seam work
   // best (FillBoundary plans, measured), long streaming task lists
@@ -1193,13 +1234,13 @@ int ghx_exec_run(ghx_exec *ex, void *const *ptrs, int64_t nptrs, void *stream) {
   int ld = ex->ld_mode;
   if (ld == 0 && !ex->nc_loads) ld = 2;  // sources may alias destinations (ParallelCopy): no .nc
   if (ex->nring) {  // ring tasks present: the ring-capable instantiation
-    ghx_copy_kernel<2, true><<<ex->blocks, ex->threads, 0, st>>>(ex->dtags, ex->dtasks, ntasks, ex->dchain, ex->dcounter, batch);
+    ghx_copy_kernel<2, true><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, ex->dcounter, batch);
   } else switch (ld) {
-    case 0: ghx_copy_kernel<0><<<ex->blocks, ex->threads, 0, st>>>(ex->dtags, ex->dtasks, ntasks, ex->dchain, ex->dcounter, batch); break;
-    case 1: ghx_copy_kernel<1><<<ex->blocks, ex->threads, 0, st>>>(ex->dtags, ex->dtasks, ntasks, ex->dchain, ex->dcounter, batch); break;
-    case 2: ghx_copy_kernel<2><<<ex->blocks, ex->threads, 0, st>>>(ex->dtags, ex->dtasks, ntasks, ex->dchain, ex->dcounter, batch); break;
-    case 3: ghx_copy_kernel<3><<<ex->blocks, ex->threads, 0, st>>>(ex->dtags, ex->dtasks, ntasks, ex->dchain, ex->dcounter, batch); break;
-    default: ghx_copy_kernel<4><<<ex->blocks, ex->threads, 0, st>>>(ex->dtags, ex->dtasks, ntasks, ex->dchain, ex->dcounter, batch); break;
+    case 0: ghx_copy_kernel<0><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, ex->dcounter, batch); break;
+    case 1: ghx_copy_kernel<1><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, ex->dcounter, batch); break;
+    case 2: ghx_copy_kernel<2><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, ex->dcounter, batch); break;
+    case 3: ghx_copy_kernel<3><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, ex->dcounter, batch); break;
+    default: ghx_copy_kernel<4><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, ex->dcounter, batch); break;
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "ghx_exec_run: launch");

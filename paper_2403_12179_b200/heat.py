@@ -106,6 +106,22 @@ def _side_stream(device: int):
     return s
 
 
+def _enqueue_step(levels: list, geoms: list, dt: float, diffusivity: float, ref_ratio: int) -> list:
+    """Single rank: the whole loop body enqueued on the current stream, no
+    host wait (also what HeatLoop captures into a CUDA graph)."""
+    import torch
+    dev = levels[0][0].device
+    st = torch.cuda.current_stream(dev).cuda_stream
+    comm.prepare_fill_boundary(levels[0][0], geoms[0]).enqueue(st)
+    if len(levels) > 1:
+        fill_patch(levels[1][0], levels[0][0], geoms[1], geoms[0], ref_ratio, LINEAR, _wait=False)
+    for lv, (u, w) in enumerate(levels):
+        _stencil(u, w, dt, diffusivity, geoms[lv], "all").run()
+    if len(levels) > 1:
+        average_down(levels[1][1], levels[0][1], ref_ratio, _wait=False)
+    return [(w, u) for (u, w) in levels]
+
+
 def heat_step(levels: list, geoms: list, dt: float, diffusivity: float, ref_ratio: int = 2, backend=None,
               overlap: bool = False) -> list:
     """One step of the reference loop (heat.py:264-273) on ``levels`` =
@@ -122,6 +138,10 @@ def heat_step(levels: list, geoms: list, dt: float, diffusivity: float, ref_rati
         raise ValueError("heat_step supports one or two levels")
     dev = levels[0][0].device
     main = torch.cuda.current_stream(dev)
+    if not overlap and comm.current_ctx().nranks == 1:
+        out = _enqueue_step(levels, geoms, dt, diffusivity, ref_ratio)
+        main.synchronize()
+        return out
     if overlap:
         side = _side_stream(dev)
         ready = torch.cuda.Event()
@@ -146,3 +166,44 @@ def heat_step(levels: list, geoms: list, dt: float, diffusivity: float, ref_rati
         average_down(levels[1][1], levels[0][1], ref_ratio, backend)
     main.synchronize()
     return [(w, u) for (u, w) in levels]
+
+
+class HeatLoop:
+    """The heat loop with each step's launches replayed from a CUDA graph
+    (single rank; launch-bound multi-level steps become one graph launch).
+
+    Steps 1-2 run eagerly (they build the plans, executors, prepared
+    transfers and bind pointer tables for both (u, unew) parities); from
+    step 3 on each parity's step is captured once and replayed.  Results are
+    identical to ``heat_step`` (same kernels, same order).  With more than
+    one rank it falls back to ``heat_step``."""
+
+    def __init__(self, levels: list, geoms: list, dt: float, diffusivity: float, ref_ratio: int = 2,
+                 graphs: bool = True):
+        self.levels, self.geoms = list(levels), list(geoms)
+        self.dt, self.diffusivity, self.ref_ratio = dt, diffusivity, ref_ratio
+        self.graphs = graphs and comm.current_ctx().nranks == 1
+        self.nsteps = 0
+        self._graph = {}
+        self._after = {}
+
+    def step(self) -> list:
+        import torch
+        if not self.graphs or self.nsteps < 2:
+            self.levels = heat_step(self.levels, self.geoms, self.dt, self.diffusivity, self.ref_ratio)
+        else:
+            p = self.nsteps % 2
+            g = self._graph.get(p)
+            if g is None:
+                torch.cuda.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    self._after[p] = _enqueue_step(self.levels, self.geoms, self.dt, self.diffusivity,
+                                                   self.ref_ratio)
+                self._graph[p] = g
+            g.replay()
+            self.levels = self._after[p]
+            torch.cuda.current_stream(self.levels[0][0].device).synchronize()
+        self.nsteps += 1
+        return self.levels
+

@@ -161,3 +161,41 @@ def test_heat_step_bit_exact(name, overlap):
         got.update(res)
     for (lv, which, gi), a in got.items():
         assert np.array_equal(a, data()[f"{name}/l{lv}{which}{gi}"].ravel(order="F")), (lv, which, gi)
+
+
+@pytest.mark.gpu
+def test_heat_loop_cuda_graphs_match_eager():
+    """HeatLoop (steps 3+ replayed from CUDA graphs) == heat_step, bit for bit,
+    on a two-level problem."""
+    import paper_2403_12179_b200 as amr
+    from paper_2403_12179_b200 import heat as H
+    amr.config.set_spacedim(3)
+    cdom = amr.Box((0, 0, 0), (15, 15, 15))
+    cgeom = amr.Geometry(cdom, (0.0,) * 3, (1.0,) * 3, (True,) * 3)
+    geoms = [cgeom, cgeom.refined(2)]
+    cba = amr.decompose(cdom, 8)
+    fba = amr.decompose(amr.Box((8, 8, 8), (23, 23, 23)), 8)
+
+    def make():
+        levels = []
+        for lv, ba in enumerate((cba, fba)):
+            dm = amr.DistributionMapping([0] * len(ba))
+            u = amr.MultiFab(ba, dm, 1, 1, geoms[lv])
+            w = amr.MultiFab(ba, dm, 1, 1, geoms[lv])
+            u.fill_hash(11 + lv, geoms[lv].domain)
+            w.setval(0.0)
+            levels.append((u, w))
+        return levels
+
+    from gpu_util import bits_of
+    eager = make()
+    for _ in range(6):
+        eager = H.heat_step(eager, geoms, 1e-5, 1.0, 2)
+    loop = H.HeatLoop(make(), geoms, 1e-5, 1.0, 2)
+    for _ in range(6):
+        loop.step()
+    assert len(loop._graph) == 2
+    for (ue, we), (ug, wg) in zip(eager, loop.levels):
+        for gi in ue.local_indices:
+            assert np.array_equal(bits_of(ue.fabs[gi]), bits_of(ug.fabs[gi]))
+            assert np.array_equal(bits_of(we.fabs[gi]), bits_of(wg.fabs[gi]))

@@ -2,7 +2,7 @@
 rows 1-2): fill_patch (FillBoundary + coarse gather + interpolation) and
 average_down (restriction + ParallelCopy).
 
-    python bench_amr.py [--op fill_patch|average_down|heat] [--steps K] [--warmup W]
+    python bench_amr.py [--op fill_patch|average_down|heat|heat2] [--steps K] [--warmup W]
 
 Workload (synthetic, splitmix64 hash data): a 256^3 periodic coarse level
 cut into 64^3 boxes, ncomp 4, float64; the fine level refines the central
@@ -91,7 +91,7 @@ def run(args):
                                   f"[{PATCH_LO},{PATCH_HI}]^3 refined x{RATIO} ({len(fba)} boxes of {BOX}^3, "
                                   f"nghost {NGROW}), ncomp {NCOMP}, float64",
                       "l2": "flushed before every step (512 MiB write + 256 MiB clean read, outside the events)"}}
-    if args.op == "heat":
+    if args.op in ("heat", "heat2"):
         pass
     elif args.op == "fill_patch":
         call = lambda: A.fill_patch(fine, coarse, fgeom, cgeom, RATIO, A.LINEAR)  # noqa: E731
@@ -136,6 +136,8 @@ def run(args):
         out["cpu_baseline"] = cpu_restrict_sample()
     if args.op == "heat":
         out.update(heat_bench(args, amr, cdom, cgeom, cba, flush, clean, hbm, peak_src))
+    if args.op == "heat2":
+        out.update(heat2_bench(args, amr, cdom, cgeom, cba, fba, fgeom, flush, clean))
     out["amr_launches"] = int(N.lib.ghx_amr_launch_count())
     print(json.dumps(out), flush=True)
 
@@ -176,6 +178,38 @@ def heat_bench(args, amr, cdom, cgeom, cba, flush, clean, hbm, peak_src):
                          "achieved": round(alg / k_mean / 1e9, 1), "peak": hbm,
                          "frac": round(alg / k_mean / 1e9 / hbm, 4), "unit": "GB/s", "peak_source": peak_src,
                          "kernel_ms": round(k_mean * 1e3, 4)}}
+
+
+def heat2_bench(args, amr, cdom, cgeom, cba, fba, fgeom, flush, clean):
+    """The two-level heat step (FillBoundary, fill_patch LINEAR, stencil on
+    both levels, average_down): eager vs CUDA-graph replay (HeatLoop)."""
+    from paper_2403_12179_b200 import heat as H
+
+    def make():
+        levels = []
+        for lv, (ba, geom) in enumerate(((cba, cgeom), (fba, fgeom))):
+            dm = amr.DistributionMapping([0] * len(ba))
+            u = amr.MultiFab(ba, dm, 1, 1, geom)
+            w = amr.MultiFab(ba, dm, 1, 1, geom)
+            u.fill_hash(20261017 + lv, geom.domain)
+            w.setval(0.0)
+            levels.append((u, w))
+        return levels
+    geoms = [cgeom, fgeom]
+    state = {"levels": make()}
+
+    def eager():
+        state["levels"] = H.heat_step(state["levels"], geoms, 1e-7, 1.0, RATIO)
+    t_eager, _ = timed(eager, args.steps, args.warmup, flush, clean)
+    loop = H.HeatLoop(make(), geoms, 1e-7, 1.0, RATIO)
+    t_graph, _ = timed(loop.step, args.steps, args.warmup, flush, clean)
+    cells = sum(b.num_pts for b in cba) + sum(b.num_pts for b in fba)
+    return {"metric": "two-level heat step cells/s (FB + fill_patch + stencils + average_down)",
+            "value": round(cells / t_graph / 1e9, 3), "unit": "Gcell/s",
+            "ms_per_step": round(t_graph * 1e3, 4), "ms_per_step_eager": round(t_eager * 1e3, 4),
+            "config": {"workload": f"coarse {N_CRSE}^3 periodic / {BOX}^3 boxes + fine patch of {len(fba)} "
+                                   f"{BOX}^3 boxes at ratio {RATIO}, ncomp 1, nghost 1, float64",
+                       "l2": "flushed before every step (512 MiB write + 256 MiB clean read, outside the events)"}}
 
 
 def cpu_interp_sample(fine_mf, targets, seconds=5.0):
@@ -219,7 +253,7 @@ def cpu_restrict_sample(seconds=5.0):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--op", default="fill_patch", choices=["fill_patch", "average_down", "heat"])
+    ap.add_argument("--op", default="fill_patch", choices=["fill_patch", "average_down", "heat", "heat2"])
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     args = ap.parse_args()

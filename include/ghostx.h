@@ -137,6 +137,10 @@ int ghx_exec_detail(const ghx_exec *ex, int64_t out[8]);
  * on HBM the sector-swap chains are faster).  Only before the first run. */
 int ghx_exec_set_ring(ghx_exec *ex, int32_t on);
 
+/* Task mix: out[6] = copy tasks, sector-swap tasks, x-line chain tasks,
+ * seam-chunk ring tasks, ring mode on, fab-local order on. */
+int ghx_exec_task_kinds(const ghx_exec *ex, int64_t out[6]);
+
 /* Launch-time tuning knob (warps per block * blocks): 0 = default. */
 int ghx_exec_set_grid(ghx_exec *ex, int32_t blocks, int32_t threads);
 

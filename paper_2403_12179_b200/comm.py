@@ -467,6 +467,10 @@ class Executor:
         N.check(N.lib.ghx_exec_detail(h, N.i64p(det)))
         self.detail = dict(zip(("tags", "tasks", "elems", "alg_bytes", "mirror_tags", "swap_tags", "blocks",
                                 "ld_mode"), (int(v) for v in det)))
+        kinds = np.zeros(6, np.int64)
+        N.check(N.lib.ghx_exec_task_kinds(h, N.i64p(kinds)))
+        self.detail.update(zip(("copy_tasks", "swap_tasks", "chain_tasks", "ring_tasks", "ring_mode", "fab_local"),
+                               (int(v) for v in kinds)))
 
     def run(self, table: np.ndarray, stream: int) -> None:
         assert table.dtype == np.uint64 and table.size == self.nptrs

@@ -1144,6 +1144,27 @@ int ghx_exec_detail(const ghx_exec *ex, int64_t out[8]) {
   return GHX_OK;
 }
 
+int ghx_exec_task_kinds(const ghx_exec *ex, int64_t out[6]) {
+  if (!ex || !out) {
+    set_error("ghx_exec_task_kinds: bad arguments");
+    return GHX_EINVAL;
+  }
+  for (int i = 0; i < 6; ++i) out[i] = 0;
+  for (const int4 &t : ex->htasks) {
+    if (t.z == -4)
+      out[3] += 1;
+    else if (t.z == -3)
+      out[2] += 1;
+    else if (t.z == -2)
+      out[1] += 1;
+    else
+      out[0] += 1;
+  }
+  out[4] = ex->ring ? 1 : 0;
+  out[5] = ex->fab_local ? 1 : 0;
+  return GHX_OK;
+}
+
 int ghx_exec_buffer_elems(const ghx_exec *ex, int64_t *per_peer) {
   if (!ex || !per_peer) {
     set_error("ghx_exec_buffer_elems: bad arguments");

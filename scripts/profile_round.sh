@@ -27,7 +27,7 @@ done
 timeout 600 python bench.py --impl reference --steps 20 --warmup 3 > gpurun_out/prof/bench_ref_C2.json 2> gpurun_out/prof/bench_ref_C2.log
 echo "bench ref rc=$?"
 # level transfers
-for op in fill_patch average_down heat; do
+for op in fill_patch average_down heat heat2; do
   timeout 600 python bench_amr.py --op $op > gpurun_out/prof/bench_amr_$op.json 2> gpurun_out/prof/bench_amr_$op.log
   echo "bench_amr $op rc=$?"
 done

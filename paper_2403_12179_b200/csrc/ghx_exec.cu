@@ -376,6 +376,58 @@ __device__ __forceinline__ void ring_task(const DevTag *__restrict__ tags, const
   }
 }
 
+// Bulk-row task (TMA 1-D bulk copies): rows of a 16-byte-vector tag are
+// moved global -> shared -> global by the copy engine of the SM, one lane
+// per row (cp.async.bulk with an mbarrier per warp), so a warp keeps
+// kBulkBytes in flight without holding them in registers.  Only for tags
+// whose source and destination do not alias (FillBoundary).
+constexpr int kBulkBytes = 8192;  // per-warp staging buffer (dynamic shared memory)
+
+__device__ __forceinline__ void bulk_task(const DevTag &t, uint32_t r0, uint32_t nrows, int lane, char *sbuf,
+                                          uint64_t *bar, uint32_t &phase) {
+  const uint32_t row_bytes = t.nxv << 4;
+  const uint32_t sbuf_s = (uint32_t)__cvta_generic_to_shared(sbuf);
+  const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(bar);
+  const uint32_t per = kBulkBytes / row_bytes;
+  for (uint32_t b0 = 0; b0 < nrows; b0 += per) {
+    const uint32_t n = min(per, nrows - b0);
+    // previous batch's stores must have read the buffer before it is refilled
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    __syncwarp();
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_s), "r"(n * row_bytes)
+                   : "memory");
+    __syncwarp();
+    const uint32_t r = r0 + b0 + (uint32_t)lane;
+    int64_t soff = 0, doff = 0;
+    if ((uint32_t)lane < n) {
+      const uint32_t q = fdiv(r, t.ny, t.my, t.sy);
+      const uint32_t c = fdiv(q, t.nz, t.mz, t.sz);
+      const uint32_t y = r - q * t.ny, z = q - c * t.nz;
+      soff = ((int64_t)y * t.src_sy + (int64_t)z * t.src_sz + (int64_t)c * t.src_sc) << 4;
+      doff = ((int64_t)y * t.dst_sy + (int64_t)z * t.dst_sz + (int64_t)c * t.dst_sc) << 4;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              sbuf_s + lane * row_bytes),
+          "l"(t.src + soff), "r"(row_bytes), "r"(bar_s)
+          : "memory");
+    }
+    uint32_t done = 0;
+    while (!done)
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(done)
+                   : "r"(bar_s), "r"(phase)
+                   : "memory");
+    phase ^= 1;
+    if ((uint32_t)lane < n) {
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(t.dst + doff),
+                   "r"(sbuf_s + lane * row_bytes), "r"(row_bytes)
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  }
+}
+
 // cooperative 112-byte descriptor load into this warp's shared slot
 __device__ __forceinline__ void fetch_tag(const DevTag *__restrict__ tags, int idx, DevTag *slot, int lane) {
   if (lane < kTagVec)
@@ -398,7 +450,7 @@ __global__ void ghx_bind_kernel(DevTag *tags, int ntags, void *const *__restrict
 // per-executor counter (counter[0]); every warp counts itself out in
 // counter[1] and the last one resets both, so the next launch (stream
 // ordered) starts from zero without a memset.  Heavy tasks come first.
-template <int LD, bool RING = false>
+template <int LD, bool RING = false, bool BULK = false>
 __global__ void __launch_bounds__(kThreads, GHX_MINB) ghx_copy_kernel(const DevTag *__restrict__ tags,
                                                             const int4 *__restrict__ tasks, int ntasks,
                                                             const int *__restrict__ chains,
@@ -412,6 +464,16 @@ __global__ void __launch_bounds__(kThreads, GHX_MINB) ghx_copy_kernel(const DevT
   DevTag &tb = slots[wib][1];
   int have_a = -1, have_b = -1;
   if (lane < kSwapSlots) swc_id[wib][lane] = -1;
+  extern __shared__ __align__(128) char bulk_smem[];  // BULK: kWarps x kBulkBytes
+  __shared__ __align__(8) uint64_t bulk_bar[kWarps];
+  uint32_t bulk_phase = 0;
+  if (BULK) {
+    if (lane == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&bulk_bar[wib])));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+  }
   __syncwarp();
   unsigned long long nb = 0;
   if (lane == 0) nb = atomicAdd(counter, (unsigned long long)batch);
@@ -430,6 +492,15 @@ __global__ void __launch_bounds__(kThreads, GHX_MINB) ghx_copy_kernel(const DevT
         chain_task<LD>(tags, chains, tk.x, tk.w, (uint32_t)tk.y, kChainRows, lane);
       } else if (RING && tk.z == -4) {  // ring task: seam chunks of 32/(2k) columns of one x-ring
         ring_task<LD>(tags, chains, tk.x, tk.w, tk.y, lane);
+      } else if (BULK && tk.z == -5) {  // bulk-row task: tk.w rows of tag tk.x from row tk.y
+        if (tk.x != have_a || have_b != -5) {
+          __syncwarp();
+          fetch_tag(tags, tk.x, &ta, lane);
+          have_a = tk.x;
+          have_b = -5;
+          __syncwarp();
+        }
+        bulk_task(ta, (uint32_t)tk.y, (uint32_t)tk.w, lane, bulk_smem + wib * kBulkBytes, &bulk_bar[wib], bulk_phase);
       } else if (tk.z == -2) {  // sector-swap task over one chunk of T1
         const int sl = tk.x & (kSwapSlots - 1);
         if (swc_id[wib][sl] != tk.x) {
@@ -463,6 +534,7 @@ __global__ void __launch_bounds__(kThreads, GHX_MINB) ghx_copy_kernel(const DevT
     }
     nb = __shfl_sync(0xffffffffu, nb, 0);
   }
+  if (BULK) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // this lane's bulk stores are done
   if (lane == 0) {
     const unsigned long long total = (unsigned long long)gridDim.x * (blockDim.x >> 5);
     if (atomicAdd(counter + 1, 1ull) == total - 1) {
@@ -549,6 +621,8 @@ struct ghx_exec {
   int64_t npaired = 0, nswap = 0;
   bool ring = false;    // x-face seams as ring tasks (coalesced 64-B chunks)
   bool fab_local = false;  // small fabs: per-tag swaps in destination-fab order, no chains
+  bool bulk = false;       // wide 16-byte-vector rows as TMA bulk-row tasks
+  int64_t nbulk = 0;
   int64_t nring = 0;
   std::vector<uint8_t> swap_fab;  // fabs touched by sector-swap tasks
   std::vector<int64_t> buf_elems;  // per peer (pack: send, unpack: recv)
@@ -729,6 +803,20 @@ void build_tasks(ghx_exec *ex) {
   ex->swap_fab.clear();
   const bool allow_swap = std::getenv("GHX_NO_SWAP") == nullptr;
   std::vector<int32_t> swap_lo;  // low tag of every sector-swap pair
+  ex->nbulk = 0;
+  auto bulk_ok = [&](size_t i) {
+    const DevTag &t = ex->htags[i];
+    const uint32_t rb = t.nxv << 4;
+    return ex->bulk && !ex->hremote[i] && t.vlog == 4 && rb >= 256 && rb <= (uint32_t)kBulkBytes &&
+           ex->kind <= GHX_EXEC_LOCAL;
+  };
+  auto emit_bulk = [&](size_t i, std::vector<int4> &out) {
+    const DevTag &t = ex->htags[i];
+    const uint32_t rows = t.nvec / t.nxv, per = std::min<uint32_t>(32, kBulkBytes / (t.nxv << 4));
+    const uint32_t step = per * 2;  // two buffer fills per task
+    for (uint32_t r = 0; r < rows; r += step) out.push_back(make_int4((int)i, (int)r, -5, (int)std::min(step, rows - r)));
+    ex->nbulk += 1;
+  };
   for (size_t i = 0; i < n; ++i) {
     const uint32_t nv = ex->htags[i].nvec;
     auto &out = ex->hremote[i] ? rem : loc;
@@ -744,7 +832,14 @@ void build_tasks(ghx_exec *ex) {
         continue;
       }
       ex->npaired += 2;
+      if (bulk_ok(i) && bulk_ok(mate[i])) {
+        emit_bulk(i, out);
+        emit_bulk(mate[i], out);
+        continue;
+      }
       for (uint32_t s = 0; s < nv; s += kChunk) out.push_back(make_int4((int)i, (int)s, mate[i], (int)s));
+    } else if (bulk_ok(i)) {
+      emit_bulk(i, out);
     } else {
       for (uint32_t s = 0; s < nv; s += 2 * kChunk)
         out.push_back(make_int4((int)i, (int)s, s + kChunk < nv ? (int)i : -1, (int)(s + kChunk)));
@@ -814,7 +909,12 @@ void build_tasks(ghx_exec *ex) {
     }
     // spread the latency-bound seam work over the launch so it overlaps the
     // bandwidth-bound row copies
-    if (std::getenv("GHX_NO_INTERLEAVE")) {
+    if (std::getenv("GHX_BULK_FIRST")) {  // experiment: bulk face rows first, then the seams
+      loc.insert(loc.end(), swaps.begin(), swaps.end());
+      swaps.clear();
+    } else if (std::getenv("GHX_NO_INTERLEAVE") || ex->nbulk) {
+      // bulk (TMA) face rows and latency-bound seams interfere when
+      // interleaved (measured); seams first, then the bulk rows
       swaps.insert(swaps.end(), loc.begin(), loc.end());
       loc.swap(swaps);
       swaps.clear();
@@ -1024,6 +1124,10 @@ int ghx_exec_create(const ghx_plan *plan, int32_t rank, int32_t kind, const int6
     }
     ex->fab_local = plan->mode == GHX_MODE_FILL_BOUNDARY && plan->ndst > 0 && bytes / plan->ndst < 64.0 * (1 << 20);
     if (const char *v = std::getenv("GHX_FAB_LOCAL")) ex->fab_local = std::atoi(v) != 0;
+    // TMA bulk rows for the wide face rows of large-fab FillBoundary (C3:
+    // -3.6 %; small fabs keep the fab-local LSU order, which bulk rows slow)
+    ex->bulk = plan->mode == GHX_MODE_FILL_BOUNDARY && !ex->fab_local;
+    if (const char *v = std::getenv("GHX_BULK")) ex->bulk = plan->mode == GHX_MODE_FILL_BOUNDARY && std::atoi(v) != 0;
   }
   build_tasks(ex);
   if (ex->htasks.size() >= (size_t)INT32_MAX / 2) {
@@ -1254,7 +1358,16 @@ int ghx_exec_run(ghx_exec *ex, void *const *ptrs, int64_t nptrs, void *stream) {
   if (const char *v = std::getenv("GHX_BATCH")) batch = std::max(1, std::atoi(v));
   int ld = ex->ld_mode;
   if (ld == 0 && !ex->nc_loads) ld = 2;  // sources may alias destinations (ParallelCopy): no .nc
-  if (ex->nring) {  // ring tasks present: the ring-capable instantiation
+  if (ex->nbulk && !ex->nring) {
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaFuncSetAttribute(ghx_copy_kernel<2, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kWarps * kBulkBytes);
+      attr_set = true;
+    }
+    ghx_copy_kernel<2, false, true><<<ex->blocks, ex->threads, kWarps * kBulkBytes, st>>>(
+        dtags, ex->dtasks, ntasks, ex->dchain, ex->dcounter, batch);
+  } else if (ex->nring) {  // ring tasks present: the ring-capable instantiation
     ghx_copy_kernel<2, true><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, ex->dcounter, batch);
   } else switch (ld) {
     case 0: ghx_copy_kernel<0><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, ex->dcounter, batch); break;

@@ -29,8 +29,17 @@ def _domain(amr, c, key="domain"):
     return amr.Box(c[key][0][:d], c[key][1][:d])
 
 
+# task-building variants of the fused kernel: default heuristics, x-line
+# chains + TMA bulk face rows (the large-fab path), fab-local swaps
+VARIANTS = {"default": {}, "chains_bulk": {"GHX_FAB_LOCAL": "0", "GHX_BULK": "1"},
+            "fab_local": {"GHX_FAB_LOCAL": "1", "GHX_BULK": "0"}}
+
+
+@pytest.mark.parametrize("variant", sorted(VARIANTS))
 @pytest.mark.parametrize("name", gu.names("fill_boundary", store="bits"))
-def test_fill_boundary_matches_reference_golden(name):
+def test_fill_boundary_matches_reference_golden(name, variant, monkeypatch):
+    for k, v in VARIANTS[variant].items():
+        monkeypatch.setenv(k, v)
     amr = _amr()
     c = gu.case(name)
     d = gu.data()
@@ -152,13 +161,16 @@ def test_c1_matches_reference_digests(G):
     assert {str(k): v for k, v in got.items()} == c["fab_sha256"]
 
 
+@pytest.mark.parametrize("variant", ["default", "chains_bulk", "fab_local"])
 @pytest.mark.parametrize("cfg", [("C2", 256, 64, 4, 2), ("C3", 512, 128, 8, 2), ("C4", 256, 16, 4, 2)])
-def test_full_size_fill_boundary_wrapped_property(cfg):
+def test_full_size_fill_boundary_wrapped_property(cfg, variant, monkeypatch):
     """At BASELINE.json's full sizes: after FillBoundary on a fully periodic
     domain every storage cell of every fab equals the hash of its periodically
     wrapped cell (the reference acceptance oracle's global-array wrap,
     tests/test_acceptance.py:112-134), valid cells unchanged."""
     import torch
+    for k, v in VARIANTS[variant].items():
+        monkeypatch.setenv(k, v)
     amr = _amr()
     name, n, b, nc, ng = cfg
     dom, geom, ba, dm = _scale_layout(amr, n, b, 1)

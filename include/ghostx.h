@@ -137,6 +137,13 @@ int ghx_exec_detail(const ghx_exec *ex, int64_t out[8]);
  * on HBM the sector-swap chains are faster).  Only before the first run. */
 int ghx_exec_set_ring(ghx_exec *ex, int32_t on);
 
+/* TMA bulk-row tasks (cp.async.bulk through shared memory) for wide rows
+ * (256 B - 8 KB, 16-byte aligned).  Default: on for FillBoundary of large
+ * fabs; for ParallelCopy only when the caller guarantees that no source
+ * byte is written by the same run (distinct MultiFabs).  Only before the
+ * first run. */
+int ghx_exec_set_bulk(ghx_exec *ex, int32_t on);
+
 /* Task mix: out[6] = copy tasks, sector-swap tasks, x-line chain tasks,
  * seam-chunk ring tasks, ring mode on, fab-local order on. */
 int ghx_exec_task_kinds(const ghx_exec *ex, int64_t out[6]);

@@ -415,13 +415,17 @@ class CommPlan:
         # fabs in pinned host memory: seam-chunk (ring) tasks, fewer and larger PCIe transactions
         host = getattr(dst_mf, "memory", "device") == "pinned" or getattr(src_mf, "memory", "device") == "pinned"
         ring = {"1": True, "0": False}.get(os.environ.get("GHX_RING", ""), host)
+        # distinct source and destination storage: no byte is read after being
+        # written in one run, so wide rows may go through TMA bulk copies
+        bulk = src_mf is not dst_mf and not host and os.environ.get("GHX_PC_BULK", "1") == "1"
         key = (rank, kind, src_mf.ngrow.comps, src_mf.ncomp, dst_mf.ngrow.comps, dst_mf.ncomp,
-               scomp, dcomp, ncomp, dst_mf.dtype.itemsize, dst_mf.device, ring, host)
+               scomp, dcomp, ncomp, dst_mf.dtype.itemsize, dst_mf.device, ring, host, bulk)
         with self._lock:
             ex = self._execs.get(key)
             if ex is None:
                 ex = Executor(self, rank, kind, src_mf.storage_rows(), src_mf.ncomp, dst_mf.storage_rows(),
-                              dst_mf.ncomp, scomp, dcomp, ncomp, dst_mf.dtype.itemsize, dst_mf.device, ring, host)
+                              dst_mf.ncomp, scomp, dcomp, ncomp, dst_mf.dtype.itemsize, dst_mf.device, ring, host,
+                              bulk)
                 self._execs[key] = ex
         return ex
 
@@ -440,13 +444,15 @@ class Executor:
     tag table; ``run`` is one launch of the fused copy kernel)."""
 
     def __init__(self, plan, rank, kind, src_rows, src_nc, dst_rows, dst_nc, scomp, dcomp, ncomp, item, device,
-                 ring=False, host=False):
+                 ring=False, host=False, bulk=False):
         h = C.c_void_p()
         N.check(N.lib.ghx_exec_create(plan._h, rank, kind, N.i64p(src_rows), src_nc, N.i64p(dst_rows), dst_nc,
                                       scomp, dcomp, ncomp, item, device, C.byref(h)))
         self._h = h
         if ring:
             N.check(N.lib.ghx_exec_set_ring(h, 1))
+        if bulk:
+            N.check(N.lib.ghx_exec_set_bulk(h, 1))
         if host:
             # fabs in host memory: the PCIe / IOMMU path saturates with few
             # concurrent warps and degrades with many (scattered 32-64 B

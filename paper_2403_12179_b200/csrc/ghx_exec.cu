@@ -1211,6 +1211,23 @@ int ghx_exec_set_ring(ghx_exec *ex, int32_t on) {
   return GHX_OK;
 }
 
+int ghx_exec_set_bulk(ghx_exec *ex, int32_t on) {
+  if (!ex) {
+    set_error("ghx_exec_set_bulk: null handle");
+    return GHX_EINVAL;
+  }
+  std::lock_guard<std::mutex> lk(ex->mu);
+  if (ex->uploaded) {
+    set_error("ghx_exec_set_bulk: the executor has already run");
+    return GHX_EINVAL;
+  }
+  if (ex->bulk != (on != 0)) {
+    ex->bulk = on != 0;
+    build_tasks(ex);
+  }
+  return GHX_OK;
+}
+
 int ghx_exec_set_grid(ghx_exec *ex, int32_t blocks, int32_t threads) {
   if (!ex || threads != kThreads || blocks < 0) {
     set_error("ghx_exec_set_grid: only 256-thread blocks are compiled");

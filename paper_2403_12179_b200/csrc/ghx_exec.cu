@@ -501,6 +501,8 @@ __global__ void __launch_bounds__(kThreads, GHX_MINB) ghx_copy_kernel(const DevT
           __syncwarp();
         }
         bulk_task(ta, (uint32_t)tk.y, (uint32_t)tk.w, lane, bulk_smem + wib * kBulkBytes, &bulk_bar[wib], bulk_phase);
+      } else if (tk.z < -2) {  // a task kind this instantiation does not carry: fail loudly
+        __trap();
       } else if (tk.z == -2) {  // sector-swap task over one chunk of T1
         const int sl = tk.x & (kSwapSlots - 1);
         if (swc_id[wib][sl] != tk.x) {
@@ -807,7 +809,8 @@ void build_tasks(ghx_exec *ex) {
   auto bulk_ok = [&](size_t i) {
     const DevTag &t = ex->htags[i];
     const uint32_t rb = t.nxv << 4;
-    return ex->bulk && !ex->hremote[i] && t.vlog == 4 && rb >= 256 && rb <= (uint32_t)kBulkBytes &&
+    // (not with ring tasks: one kernel instantiation carries one of the two)
+    return ex->bulk && !ex->ring && !ex->hremote[i] && t.vlog == 4 && rb >= 256 && rb <= (uint32_t)kBulkBytes &&
            ex->kind <= GHX_EXEC_LOCAL;
   };
   auto emit_bulk = [&](size_t i, std::vector<int4> &out) {
@@ -1375,7 +1378,11 @@ int ghx_exec_run(ghx_exec *ex, void *const *ptrs, int64_t nptrs, void *stream) {
   if (const char *v = std::getenv("GHX_BATCH")) batch = std::max(1, std::atoi(v));
   int ld = ex->ld_mode;
   if (ld == 0 && !ex->nc_loads) ld = 2;  // sources may alias destinations (ParallelCopy): no .nc
-  if (ex->nbulk && !ex->nring) {
+  if (ex->nbulk && ex->nring) {
+    set_error("ghx_exec_run: ring and bulk tasks in one executor");
+    return GHX_EINVAL;
+  }
+  if (ex->nbulk) {
     static bool attr_set = false;
     if (!attr_set) {
       cudaFuncSetAttribute(ghx_copy_kernel<2, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,

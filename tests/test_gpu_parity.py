@@ -273,6 +273,36 @@ def test_pinned_host_multifab_fill_boundary():
         assert gu.fab_digest(bits_of(mf.fabs[gi])) == c["fab_sha256"][str(gi)]
 
 
+@pytest.mark.parametrize("n,b,nc", [(128, 64, 2), (256, 128, 4)])
+def test_pinned_host_large_and_small_fabs_wrapped_property(n, b, nc):
+    """Host-resident fabs take the seam-chunk (ring) task path; with fabs
+    over 64 MiB (the second case) the device path would also use x-line
+    chains and TMA bulk rows -- the host executor must not mix them."""
+    import torch
+    amr = _amr()
+    amr.config.set_spacedim(3)
+    dom = amr.Box((0, 0, 0), (2 * b - 1, b - 1, b - 1)) if n == 256 else amr.Box((0, 0, 0), (n - 1,) * 3)
+    geom = amr.Geometry(dom, (0.0,) * 3, (1.0,) * 3, (True,) * 3)
+    ba = amr.decompose(dom, b)
+    dm = amr.DistributionMapping([0] * len(ba))
+    mf = amr.MultiFab(ba, dm, nc, 2, geom, memory="pinned")
+    ref = amr.MultiFab(ba, dm, nc, 2, geom)  # device twin: wrapped-hash property checked on the device
+    mf.fill_hash(inputs.SEED, dom)
+    ref.fill_hash(inputs.SEED, dom)
+    torch.cuda.synchronize()
+    amr.fill_boundary(mf, geom)
+    amr.fill_boundary(ref, geom)
+    ex = amr.comm.prepare_fill_boundary(mf, geom).ex
+    assert ex.detail["ring_tasks"] > 0 and ex.detail["ring_mode"] == 1
+    bad = 0
+    for gi in mf.local_indices:
+        exp = expected_wrapped(ref.fabs[gi], nc, dom.as_row(), (1, 1, 1), inputs.SEED, 8)
+        assert bool((device_bits(ref.fabs[gi]) == exp).all())
+        got = torch.from_numpy(bits_of(mf.fabs[gi]).view(np.int64))
+        bad += int((got != exp.cpu()).sum().item())
+    assert bad == 0
+
+
 def test_known_values_1d_and_constant_field():
     """Reference tests/test_comm.py:198-222 through the CUDA path."""
     amr = _amr()

@@ -478,8 +478,20 @@ def e2e_leg(args, amr, cfg, L, world, ghost_bytes, x):
             ts.append(time.perf_counter() - t0)
         t = statistics.median(ts)
         moved = x.ghost_bytes
+        verified = None
+        if cfg["kind"] == "fb" and hmf.local_indices:  # the host-resident result, checked like the device one
+            import ctypes as C
+            from paper_2403_12179_b200 import _native as N
+            f = hmf.fabs[hmf.local_indices[0]]
+            exp = torch.empty(f.raw().numel(), dtype=torch.int64, device="cuda")
+            N.check(N.lib.ghx_fill_hash_wrapped(
+                C.c_void_p(exp.data_ptr()), N.i64p(np.asarray(f.box.as_row(), np.int64)), hmf.ncomp,
+                N.i64p(np.asarray(L["dom"].as_row(), np.int64)), N.i32p(np.ones(3, np.int32)),
+                C.c_uint64(SEED), 8, None))
+            verified = bool(torch.equal(f.raw().view(torch.int64), exp.cpu()))
         return {"value": round(ghost_bytes / t / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": int(moved),
                 "d2h_bytes_per_step": int(moved), "ms_per_step": round(t * 1e3, 3), "steps": steps,
+                "verified": verified,
                 "path": "public fill_boundary/parallel_copy on pinned host MultiFabs: the fused kernel reads "
                         "source cells and writes ghost cells across PCIe (zero-copy, mapped memory)"}
     # N > 1: staged -- pinned host shadow of this rank's storage, H2D + exchange + D2H per step

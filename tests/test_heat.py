@@ -199,3 +199,44 @@ def test_heat_loop_cuda_graphs_match_eager():
         for gi in ue.local_indices:
             assert np.array_equal(bits_of(ue.fabs[gi]), bits_of(ug.fabs[gi]))
             assert np.array_equal(bits_of(we.fabs[gi]), bits_of(wg.fabs[gi]))
+
+
+@pytest.mark.gpu
+def test_heat_loop_rank_invariant():
+    """Reference tests/test_tools.py:215-231: the result does not depend on
+    the number of ranks (1, 2, 3 thread ranks on one GPU, two levels)."""
+    import paper_2403_12179_b200 as amr
+    from paper_2403_12179_b200 import heat as H
+    from gpu_util import bits_of
+    amr.config.set_spacedim(2)
+    cdom = amr.Box((0, 0), (31, 31))
+    cgeom = amr.Geometry(cdom, (0.0, 0.0), (1.0, 1.0), (True, True))
+    geoms = [cgeom, cgeom.refined(2)]
+    cba = amr.decompose(cdom, 8)
+    fba = amr.BoxArray([amr.Box((16, 16), (31, 39)), amr.Box((32, 16), (47, 31))])
+
+    def run(nranks):
+        def program(ctx):
+            levels = []
+            for lv, ba in enumerate((cba, fba)):
+                dm = amr.DistributionMapping.round_robin(len(ba), nranks)
+                u = amr.MultiFab(ba, dm, 1, 1, geoms[lv])
+                w = amr.MultiFab(ba, dm, 1, 1, geoms[lv])
+                u.fill_hash(5 + lv, geoms[lv].domain)
+                w.setval(0.0)
+                levels.append((u, w))
+            ctx.barrier()
+            for _ in range(3):
+                levels = H.heat_step(levels, geoms, 1e-5, 1.0, 2)
+            return {(lv, gi): bits_of(u.fabs[gi]) for lv, (u, _) in enumerate(levels) for gi in u.local_indices}
+        out = {}
+        for r in amr.runtime_spawn(nranks, program):
+            out.update(r)
+        return out
+
+    base = run(1)
+    for n in (2, 3):
+        got = run(n)
+        assert got.keys() == base.keys()
+        for k in base:
+            assert np.array_equal(got[k], base[k]), (n, k)

@@ -161,6 +161,8 @@ int ghx_memset_u64(void *ptr, uint64_t value, size_t count, void *stream);
 int ghx_enable_peer_access(int32_t device, int32_t peer);
 int ghx_ipc_get_handle(void *ptr, uint8_t handle[64]);
 int ghx_ipc_open_handle(int32_t device, const uint8_t handle[64], void **out);
+/* Byte offset of ptr inside its device allocation (IPC maps whole allocations). */
+int ghx_alloc_offset(const void *ptr, uint64_t *offset);
 int ghx_ipc_close_handle(void *ptr);
 int ghx_stream_sync(void *stream);
 

@@ -669,9 +669,15 @@ def _ipc_peers(ctx, mf: MultiFab):
         return cache
     h = (C.c_uint8 * 64)()
     have = mf._slab is not None
+    base = 0
     if have:
         N.check(N.lib.ghx_ipc_get_handle(C.c_void_p(mf._slab.ptr), h))
-    offs = [int(p) - mf._slab.ptr for p in mf._ptrs] if have else []
+        # the handle maps the whole allocation (an arena slab may hold this
+        # MultiFab's storage at an offset)
+        o = C.c_uint64()
+        N.check(N.lib.ghx_alloc_offset(C.c_void_p(mf._slab.ptr), C.byref(o)))
+        base = mf._slab.ptr - o.value
+    offs = [int(p) - base for p in mf._ptrs] if have else []
     infos = ctx.allgather((ctx.rank, bytes(h) if have else None, mf.local_indices, offs))
     parts, opened = [], []
     for (r, hb, idx, off) in infos:

@@ -239,6 +239,36 @@ int ghx_ipc_get_handle(void *ptr, uint8_t handle[64]) {
   return GHX_OK;
 }
 
+int ghx_alloc_offset(const void *ptr, uint64_t *offset) {
+  // byte offset of ptr inside its cudaMalloc allocation (a CUDA-IPC handle
+  // maps the whole allocation, so peers add this offset to the opened base)
+  if (!ptr || !offset) {
+    set_error("ghx_alloc_offset: bad arguments");
+    return GHX_EINVAL;
+  }
+  using GetRange = int (*)(unsigned long long *, size_t *, unsigned long long);
+  static GetRange fn = [] {
+    void *f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<GetRange>(f);
+  }();
+  if (!fn) {
+    set_error("ghx_alloc_offset: cuMemGetAddressRange unavailable");
+    return GHX_ECUDA;
+  }
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (fn(&base, &size, (unsigned long long)reinterpret_cast<uintptr_t>(ptr)) != 0) {
+    set_error("ghx_alloc_offset: not a device allocation");
+    return GHX_EINVAL;
+  }
+  *offset = (uint64_t)(reinterpret_cast<uintptr_t>(ptr) - base);
+  return GHX_OK;
+}
+
 int ghx_ipc_open_handle(int32_t device, const uint8_t handle[64], void **out) {
   if (!handle || !out) {
     set_error("ghx_ipc_open_handle: bad arguments");

@@ -41,7 +41,12 @@ def _worker(rank, world, port, q, n, b, nc, ng, env=None):
         geom = amr.Geometry(dom, (0.0,) * 3, (1.0,) * 3, (True,) * 3)
         ba = amr.decompose(dom, b)
         dm = amr.DistributionMapping.round_robin(len(ba), world)
-        mf = amr.MultiFab(ba, dm, nc, ng, geom)
+        arena = None
+        if os.environ.get("GHX_TEST_ARENA"):  # storage inside a pooled slab, after a 4 KiB block
+            from paper_2403_12179_b200.arena import Arena
+            arena = Arena(0)
+            arena.alloc(4096)
+        mf = amr.MultiFab(ba, dm, nc, ng, geom, arena=arena)
         mf.fill_hash(inputs.SEED, dom)
         torch.cuda.synchronize()
         ctx = amr.current_ctx()
@@ -71,11 +76,13 @@ CASES = [("C1", 64, 32, 1, 1, "C1_x2", {"GHX_REMOTE": "direct"}), ("C3", 512, 12
          ("C1", 64, 32, 1, 1, "C1_x2", {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "20"}),
          # the pack -> message -> unpack fallback (host-staged over gloo here)
          ("C1", 64, 32, 1, 1, "C1_x2", {"GHX_TRANSPORT": "nccl"}),
-         ("C3", 512, 128, 8, 2, "C3_x2", {"GHX_TRANSPORT": "nccl"})]
+         ("C3", 512, 128, 8, 2, "C3_x2", {"GHX_TRANSPORT": "nccl"}),
+         # fab storage at an offset inside an arena slab: IPC maps whole allocations
+         ("C1", 64, 32, 1, 1, "C1_x2", {"GHX_TEST_ARENA": "1", "GHX_REMOTE": "direct"})]
 
 
 @pytest.mark.parametrize("cfg", CASES, ids=["C1-ipc-direct", "C3-ipc-packed", "C3-ipc-direct", "C1-devbarrier-packed",
-                                            "C1-fallback", "C3-fallback"])
+                                            "C1-fallback", "C3-fallback", "C1-arena-ipc"])
 def test_two_processes_one_gpu(cfg):
     name, n, b, nc, ng, golden, env = cfg
     world = 2

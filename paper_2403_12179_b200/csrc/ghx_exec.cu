@@ -64,7 +64,10 @@ constexpr int kChunk = 32 * kU;     // vectors per chunk (a task has two)
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kSwapSlots = 8;
-constexpr int kChainRows = 64;  // rows per chain task
+#ifndef GHX_CHAIN_ROWS
+#define GHX_CHAIN_ROWS 64
+#endif
+constexpr int kChainRows = GHX_CHAIN_ROWS;  // rows per chain task
 #ifndef GHX_CHAIN_R
 #define GHX_CHAIN_R 2
 #endif

@@ -190,6 +190,14 @@ int ghx_fill_hash(void *fab, const int64_t fab_box[6], int32_t ncomp, const int6
 int ghx_fill_hash_wrapped(void *fab, const int64_t fab_box[6], int32_t ncomp, const int64_t domain_box[6],
                           const int32_t periodic[3], uint64_t seed, int32_t elem_bytes, void *stream);
 
+/* ------------------------------------------------------------ index copy */
+
+/* index_mapped_copy's data movement (reference comm.py:465-560): for every
+ * cell, ncomp raw words from src to dst.  d_rows: device array of ncells
+ * rows {src byte address, dst byte address, src component stride (bytes),
+ * dst component stride (bytes)}; addresses may be peer or IPC mappings. */
+int ghx_index_copy(const int64_t *d_rows, int64_t ncells, int32_t ncomp, int32_t elem_bytes, void *stream);
+
 /* ----------------------------------------------------------------- arena */
 
 /* Pooled arena (reference arena.py:87-197): slabs + LIFO free lists per

@@ -311,3 +311,33 @@ def ghost_bytes(plan, ncomp, itemsize):
     if s.shape[0] == 0:
         return 0
     return int((s[:, 5:8] - s[:, 2:5] + 1).prod(axis=1).sum()) * ncomp * itemsize
+
+
+def index_copy(dst_boxes, dst_fabs, dst_lo, src_boxes, src_fabs, src_lo, mapping_fn, region=None):
+    """index_mapped_copy (comm.py:465-560): dst(cell) = src(mapping(cell)) over
+    the dst valid cells (intersected with region), the first src valid box in
+    order owning each mapped point; all components.  Boxes padded (n, 6)."""
+    src_boxes = np.asarray(src_boxes, np.int64).reshape(-1, 6)
+    for dj, db in enumerate(np.asarray(dst_boxes, np.int64).reshape(-1, 6)):
+        w = db.copy()
+        if region is not None:
+            w = np.concatenate([np.maximum(db[:3], region[:3]), np.minimum(db[3:], region[3:])])
+        if np.any(w[3:] < w[:3]):
+            continue
+        ex = w[3:] - w[:3] + 1
+        flat = np.arange(int(np.prod(ex)), dtype=np.int64)
+        di, dy, dk = flat % ex[0] + w[0], (flat // ex[0]) % ex[1] + w[1], flat // (ex[0] * ex[1]) + w[2]
+        mi, mj, mk = (np.asarray(v, np.int64) for v in mapping_fn(di, dy, dk))
+        owner = np.full(di.size, -1, np.int64)
+        for si, sb in enumerate(src_boxes):
+            m = ((mi >= sb[0]) & (mi <= sb[3]) & (mj >= sb[1]) & (mj <= sb[4]) & (mk >= sb[2]) & (mk <= sb[5])
+                 & (owner < 0))
+            owner[m] = si
+        if (owner < 0).any():
+            raise ValueError("mapping leaves cells outside src coverage")
+        dl = dst_lo[dj]
+        for si in np.unique(owner):
+            m = owner == si
+            sl = src_lo[int(si)]
+            dst_fabs[dj][di[m] - dl[0], dy[m] - dl[1], dk[m] - dl[2], :] = \
+                src_fabs[int(si)][mi[m] - sl[0], mj[m] - sl[1], mk[m] - sl[2], :]

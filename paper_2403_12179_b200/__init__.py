@@ -21,7 +21,8 @@ from .mesh import (BoxArray, DistributionMapping, Fab, FabView, MultiFab, decomp
 
 __version__ = "0.1.0"
 from .bridge import BoundArray4, MfiAccessor, array_view, multifab_iter  # noqa: E402
-from .comm import build_gather_plan, gather_fabs, prepare_fill_boundary, prepare_parallel_copy  # noqa: E402
+from .comm import (build_gather_plan, gather_fabs, index_mapped_copy, prepare_fill_boundary,  # noqa: E402
+                   prepare_parallel_copy)
 from . import amr  # noqa: E402,F401
 from .amr import LINEAR, PIECEWISE_CONSTANT, average_down, fill_patch, interp_box  # noqa: E402,F401
 from . import heat  # noqa: E402,F401

@@ -69,6 +69,7 @@ _SIGS = {
     "ghx_ipc_open_handle": (C.c_int, [I32, C.POINTER(C.c_uint8), C.POINTER(P)]),
     "ghx_ipc_close_handle": (C.c_int, [P]),
     "ghx_alloc_offset": (C.c_int, [P, C.POINTER(C.c_uint64)]),
+    "ghx_index_copy": (C.c_int, [P, I64, I32, I32, P]),
     "ghx_stream_sync": (C.c_int, [P]),
     "ghx_signal_barrier": (C.c_int, [C.POINTER(P), I32, I32, C.c_uint64, P]),
     "ghx_barrier_timeouts": (I64, []),

@@ -40,7 +40,7 @@ import numpy as np
 
 from . import _native as N
 from . import config
-from .index_space import Box, Geometry, IntVect
+from .index_space import Box, Geometry, IntVect, grow
 from .mesh import MultiFab, Slab
 
 SUM, MIN, MAX = "sum", "min", "max"
@@ -1098,3 +1098,104 @@ def gather_targets(plan: CommPlan, dst_fabs: list, dst_ranks: list, src: MultiFa
     fs = _gather_set(plan, dst_fabs, dst_ranks, src)
     return {fid: fs.fabs[pos] for pos, (fid, _) in enumerate(dst_fabs) if pos in fs.fabs}
 
+
+
+# ---------------------------------------------------------- index-mapped copy
+
+def _box_cells(box: Box):
+    """Global (i, j, k) int64 arrays of the box's cells in F order, padded to
+    3-D (kernels.py:159-171)."""
+    from .mesh import _pad3
+    ex, ey, ez = _pad3(box.extents, 1)
+    lo = _pad3(box.lo, 0)
+    flat = np.arange(ex * ey * ez, dtype=np.int64)
+    return flat % ex + lo[0], (flat // ex) % ey + lo[1], flat // (ex * ey) + lo[2]
+
+
+def index_mapped_copy(dst: MultiFab, src: MultiFab, mapping_fn, region: Box | None = None, backend=None) -> None:
+    """dst(cell) = src(mapping_fn(cell)) over dst's valid cells (reference
+    comm.py:465-560).  ``mapping_fn`` takes (i, j, k) int64 arrays and returns
+    the mapped (i, j, k); every mapped point must lie in a src valid box
+    (the first one in BoxArray order wins), else ValueError.  The mapping is
+    evaluated on the host, redundantly on every rank (it is user Python);
+    each rank then pushes the cells it owns the sources of -- local and
+    remote destinations alike -- with one gather/scatter launch, and the
+    per-ordered-pair message accounting follows the reference."""
+    import torch
+    from .index_space import intersect
+    from .mesh import _pad3
+    if src.ba.ixtype != dst.ba.ixtype:
+        raise ValueError("index_mapped_copy requires matching index types")
+    if src.ncomp != dst.ncomp:
+        raise ValueError("index_mapped_copy requires matching component counts")
+    if src.dtype != dst.dtype:
+        raise ValueError("index_mapped_copy requires matching real types")
+    ctx = current_ctx()
+    me = ctx.rank
+    slo = np.asarray([_pad3(b.lo, 0) for b in src.ba], np.int64).reshape(-1, 3)
+    shi = np.asarray([_pad3(b.hi, 0) for b in src.ba], np.int64).reshape(-1, 3)
+    jobs = []  # (src fab, dst fab, mapped coords, dst coords) with src rank == me
+    pair_cells: dict = {}
+    for dj, dbox in enumerate(dst.ba):
+        work = dbox if region is None else intersect(dbox, region)
+        if work.is_empty:
+            continue
+        di, dy, dk = _box_cells(work)
+        mi, mj, mk = (np.asarray(v, dtype=np.int64) for v in mapping_fn(di, dy, dk))
+        owner = np.full(di.size, -1, np.int64)
+        for si in range(len(src.ba)):
+            m = ((mi >= slo[si, 0]) & (mi <= shi[si, 0]) & (mj >= slo[si, 1]) & (mj <= shi[si, 1])
+                 & (mk >= slo[si, 2]) & (mk <= shi[si, 2]) & (owner < 0))
+            owner[m] = si
+        if (owner < 0).any():
+            raise ValueError(f"mapping leaves {int((owner < 0).sum())} cells of dst fab {dj} outside src coverage")
+        dr = dst.dm[dj]
+        for si in np.unique(owner):
+            sr = src.dm[int(si)]
+            m = owner == si
+            pair_cells[(sr, dr)] = pair_cells.get((sr, dr), 0) + int(m.sum())
+            if sr == me:
+                jobs.append((int(si), dj, (mi[m], mj[m], mk[m]), (di[m], dy[m], dk[m])))
+    # destination pointers of every rank's fabs
+    if ctx.nranks == 1:
+        dptr = dict(zip(dst.local_indices, (int(p) for p in dst._ptrs)))
+    elif ctx.kind == "process":
+        dptr = {}
+        for idx, ptrs in _ipc_peers(ctx, dst):
+            dptr.update(zip(idx, (int(p) for p in ptrs)))
+    else:
+        torch.cuda.current_stream(dst.device).synchronize()  # peers may still work on their fabs
+        dptr = {}
+        for (_, d, idx, ptrs) in ctx.allgather((me, dst.device, dst.local_indices, dst._ptrs)):
+            if d != dst.device and (dst.device, d) not in _peer_enabled:
+                N.check(N.lib.ghx_enable_peer_access(dst.device, d))
+                _peer_enabled.add((dst.device, d))
+            dptr.update(zip(idx, (int(p) for p in ptrs)))
+    if ctx.kind == "process" and ctx.nranks > 1:
+        torch.cuda.current_stream(dst.device).synchronize()
+        ctx.barrier()  # peers finished earlier work on the fabs this rank writes
+    item = dst.dtype.itemsize
+    rows = []
+    for si, dj, (mi, mj, mk), (di, dy, dk) in jobs:
+        sf = src.fabs[si]
+        sb_lo, sn = _pad3(sf.box.lo, 0), _pad3(sf.box.extents, 1)
+        db = grow(dst.ba[dj], dst.ngrow)
+        db_lo, dn = _pad3(db.lo, 0), _pad3(db.extents, 1)
+        soff = (mi - sb_lo[0]) + sn[0] * ((mj - sb_lo[1]) + sn[1] * (mk - sb_lo[2]))
+        doff = (di - db_lo[0]) + dn[0] * ((dy - db_lo[1]) + dn[1] * (dk - db_lo[2]))
+        r = np.empty((soff.size, 4), np.int64)
+        r[:, 0] = np.uint64(sf.ptr).view(np.int64) + soff * item
+        r[:, 1] = np.uint64(dptr[dj]).view(np.int64) + doff * item
+        r[:, 2] = sn[0] * sn[1] * sn[2] * item
+        r[:, 3] = dn[0] * dn[1] * dn[2] * item
+        rows.append(r)
+    stream = torch.cuda.current_stream(src.device)
+    if rows:
+        table = torch.from_numpy(np.ascontiguousarray(np.concatenate(rows))).to(f"cuda:{src.device}")
+        N.check(N.lib.ghx_index_copy(C.c_void_p(table.data_ptr()), table.shape[0], src.ncomp, item,
+                                     C.c_void_p(stream.cuda_stream)))
+    stream.synchronize()
+    for (sr, dr), cells in sorted(pair_cells.items()):
+        if sr == me and dr != me:
+            ctx.bus.account(sr, dr, cells * src.ncomp * item)
+    ctx.barrier()

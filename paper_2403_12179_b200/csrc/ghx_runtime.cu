@@ -4,6 +4,7 @@
 // can address local fabs, peer-mapped fabs and IPC-mapped fabs uniformly.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -374,3 +375,44 @@ int ghx_fill_hash_wrapped(void *fab, const int64_t fab_box[6], int32_t ncomp, co
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------ index copy
+
+namespace {
+
+// One thread per (cell, component): rows = {src byte address, dst byte
+// address, src component stride, dst component stride} per cell; raw words.
+template <class W>
+__global__ void index_copy_kernel(const int64_t *__restrict__ rows, int64_t n, int ncomp) {
+  const int64_t total = n * ncomp;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t cell = i % n, c = i / n;
+    const int64_t *r = rows + 4 * cell;
+    const W v = *reinterpret_cast<const W *>(r[0] + c * r[2]);
+    *reinterpret_cast<W *>(r[1] + c * r[3]) = v;
+  }
+}
+
+}  // namespace
+
+extern "C" int ghx_index_copy(const int64_t *d_rows, int64_t ncells, int32_t ncomp, int32_t elem_bytes,
+                              void *stream) {
+  if ((ncells && !d_rows) || ncells < 0 || ncomp < 1 || (elem_bytes != 4 && elem_bytes != 8)) {
+    set_error("ghx_index_copy: bad arguments");
+    return GHX_EINVAL;
+  }
+  if (ncells == 0) return GHX_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t want = (ncells * ncomp + 255) / 256;
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * 8));
+  if (elem_bytes == 8)
+    index_copy_kernel<uint64_t><<<blocks, 256, 0, st>>>(d_rows, ncells, ncomp);
+  else
+    index_copy_kernel<uint32_t><<<blocks, 256, 0, st>>>(d_rows, ncells, ncomp);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(e, "ghx_index_copy");
+  return GHX_OK;
+}

@@ -308,12 +308,72 @@ def gen_heat(rng):
     run_heat("heat_2l_3d", 3, [8, 8, 8], 4, [Box((4, 4, 4), (11, 11, 11))], 2, 2, 2, 1e-5, 1.0, np.float64)
 
 
+# ------------------------------------------------------- index_mapped_copy
+
+MAPPINGS = {
+    "identity": lambda n: (lambda i, j, k: (i, j, k)),
+    "reflect_x": lambda n: (lambda i, j, k: (n[0] - 1 - i, j, k)),
+    "shift_wrap": lambda n: (lambda i, j, k: ((i + 3) % n[0], (j + 5) % n[1], k)),
+    "transpose_xy": lambda n: (lambda i, j, k: (j, i, k)),
+}
+
+
+def run_index_copy(name, dim, ext, smgs, dmgs, nranks, ncomp, sng, dng, mapping, region, dtype):
+    set_cfg(dim, dtype)
+    dom = Box([0] * dim, [e - 1 for e in ext])
+    sba, dba = decompose(dom, smgs), decompose(dom, dmgs)
+    sdm = DistributionMapping([i % nranks for i in range(len(sba))], nranks)
+    ddm = DistributionMapping([(i + 1) % nranks for i in range(len(dba))], nranks)
+    fn = MAPPINGS[mapping](pad3(ext, 1))
+    reg = None if region is None else Box(region[0][:dim], region[1][:dim])
+
+    def program(ctx):
+        src = MultiFab(sba, sdm, ncomp, sng)
+        dst = MultiFab(dba, ddm, ncomp, dng)
+        for gi in src.local_indices:
+            fill(src.fabs[gi], sba[gi], dom, inputs.SEED)
+        for gi in dst.local_indices:
+            fill(dst.fabs[gi], dba[gi], dom, SEED_C)
+        ctx.barrier()
+        s0 = ctx.bus.stats_snapshot()
+        ctx.barrier()  # no rank sends before every rank took its snapshot
+        comm.index_mapped_copy(dst, src, fn, region=reg, backend=Backend("serial"))
+        ctx.barrier()  # every rank's sends are in the Bus stats
+        s1 = ctx.bus.stats_snapshot()
+        stats = {f"{a}->{b}": (s1[(a, b)][0] - s0[(a, b)][0], s1[(a, b)][1] - s0[(a, b)][1])
+                 for (a, b) in s1 if s1[(a, b)] != s0[(a, b)]}
+        return {gi: inputs.bits(dst.fabs[gi].data).copy(order="F") for gi in dst.local_indices}, stats
+
+    res = comm.runtime_spawn(nranks, program)
+    for out, _ in res:
+        for gi, a in out.items():
+            ARRAYS[f"{name}/dst{gi}"] = a
+    CASES.append(dict(name=name, kind="index_copy", dim=dim, ext=pad3(ext, 1), smgs=smgs, dmgs=dmgs, nranks=nranks,
+                      ncomp=ncomp, sng=sng, dng=dng, mapping=mapping,
+                      region=None if region is None else [pad3(region[0]), pad3(region[1])],
+                      dtype=np.dtype(dtype).name, stats=res[0][1],
+                      src_boxes=[box6(b) for b in sba], src_rank=list(sdm.rank_of),
+                      dst_boxes=[box6(b) for b in dba], dst_rank=list(ddm.rank_of)))
+    reset_cfg()
+
+
+def gen_index_copy():
+    run_index_copy("imc_identity_1d", 1, [16], 8, 8, 1, 1, 0, 0, "identity", None, np.float64)
+    run_index_copy("imc_reflect_1d_2r", 1, [24], 8, 6, 2, 2, 0, 1, "reflect_x", None, np.float64)
+    run_index_copy("imc_shift_2d", 2, [12, 10], 5, 4, 1, 2, 1, 1, "shift_wrap", None, np.float64)
+    run_index_copy("imc_shift_2d_2r", 2, [12, 10], 6, 5, 2, 1, 0, 2, "shift_wrap", ([1, 2], [9, 8]), np.float32)
+    run_index_copy("imc_transpose_3d_2r", 3, [8, 8, 6], 4, 3, 2, 2, 1, 0, "transpose_xy", None, np.float64)
+    run_index_copy("imc_reflect_3d", 3, [10, 6, 6], 4, 5, 1, 3, 0, 0, "reflect_x", ([2, 0, 1], [8, 5, 4]),
+                   np.float64)
+
+
 def main():
     rng = np.random.default_rng(20261017)
     gen_interp(rng, 30)
     gen_avgdown(rng, 18)
     gen_fill_patch(rng, 18)
     gen_heat(rng)
+    gen_index_copy()
     with open(os.path.join(HERE, "golden_amr.json"), "w") as f:
         json.dump({"generator": "tests/golden/make_golden_amr.py", "reference": "miniamr_core (amr.py)",
                    "seed_fine": inputs.SEED, "seed_crse": SEED_C, "cases": CASES}, f, indent=0)

@@ -43,19 +43,35 @@ def _worker(rank, world, port, q, name):
         from oracle import inputs
         from test_amr_oracle import grown, hashed, meta
         c = case(name)
-        dim, dt, r = c["dim"], np.dtype(c["dtype"]), c["ratio"]
+        dim, dt, r = c["dim"], np.dtype(c["dtype"]), c.get("ratio", 1)
         amr.config.set_spacedim(dim)
         amr.config.set_real_dtype(dt)
         box = lambda b6: amr.Box(tuple(b6[:dim]), tuple(b6[3:3 + dim]))  # noqa: E731
-        cdom6 = [0, 0, 0] + [e - 1 for e in c["cext"]]
-        fdom6 = [0, 0, 0] + [e * (r if d < dim else 1) - 1 for d, e in enumerate(c["cext"])]
-        per = tuple(bool(p) for p in c.get("periodic", [True] * 3)[:dim])
-        cgeom = amr.Geometry(box(cdom6), (0.0,) * dim, (1.0,) * dim, per)
-        fgeom = cgeom.refined(r)
-        cba = amr.BoxArray([box(b) for b in c["crse_boxes"]])
-        cdm = amr.DistributionMapping(c["crse_rank"], c["nranks"])
+        if c["kind"] != "index_copy":
+            cdom6 = [0, 0, 0] + [e - 1 for e in c["cext"]]
+            fdom6 = [0, 0, 0] + [e * (r if d < dim else 1) - 1 for d, e in enumerate(c["cext"])]
+            per = tuple(bool(p) for p in c.get("periodic", [True] * 3)[:dim])
+            cgeom = amr.Geometry(box(cdom6), (0.0,) * dim, (1.0,) * dim, per)
+            fgeom = cgeom.refined(r)
+            cba = amr.BoxArray([box(b) for b in c["crse_boxes"]])
+            cdm = amr.DistributionMapping(c["crse_rank"], c["nranks"])
         out = {}
-        if c["kind"] == "heat":
+        if c["kind"] == "index_copy":
+            from test_index_copy import MAPPINGS, _inputs
+            sba = amr.BoxArray([box(b) for b in c["src_boxes"]])
+            dba = amr.BoxArray([box(b) for b in c["dst_boxes"]])
+            src = amr.MultiFab(sba, amr.DistributionMapping(c["src_rank"], c["nranks"]), c["ncomp"], c["sng"])
+            dst = amr.MultiFab(dba, amr.DistributionMapping(c["dst_rank"], c["nranks"]), c["ncomp"], c["dng"])
+            hsrc, hdst = _inputs(c)
+            for gi in src.local_indices:
+                upload(src.fabs[gi], hsrc[gi])
+            for gi in dst.local_indices:
+                upload(dst.fabs[gi], hdst[gi])
+            dist.barrier()
+            region = None if c["region"] is None else amr.Box(tuple(c["region"][0][:dim]), tuple(c["region"][1][:dim]))
+            amr.index_mapped_copy(dst, src, MAPPINGS[c["mapping"]](c["ext"]), region=region)
+            out = {f"dst{gi}": bits_of(dst.fabs[gi]) for gi in dst.local_indices}
+        elif c["kind"] == "heat":
             specs = [(cba, cdm)]
             if c["fine_boxes"]:
                 specs.append((amr.BoxArray([box(b) for b in c["fine_boxes"]]),
@@ -110,7 +126,7 @@ def _worker(rank, world, port, q, name):
 
 
 # three 2-rank cases per kind keep the suite short (each case spawns two processes)
-TWO_RANK = [n for kind in ("fill_patch", "average_down", "heat")
+TWO_RANK = [n for kind in ("fill_patch", "average_down", "heat", "index_copy")
             for n in [m for m in names(kind) if case(m)["nranks"] == 2][:3]]
 
 

@@ -293,6 +293,48 @@ def cpu_sample(cfg, seconds=10.0, max_reps=200, workers=None, reps=None, budget=
     return nbytes / statistics.median(times) / 1e9, desc, times, nbytes, workers
 
 
+def cpu_sample_interp(fine_mf, targets, NCOMP, NGROW, RATIO, seconds=5.0):
+    """cpu_baseline leg of bench_amr.py --op fill_patch: the numpy oracle of
+    interp_box (reference amr.py:269-314 arithmetic) on the first regions."""
+    import paper_2403_12179_b200 as amr
+    from oracle import amr_oracle as ao
+    rng = np.random.default_rng(1)
+    t0 = time.perf_counter()
+    done = 0
+    jobs = [(gi, r) for gi in sorted(targets) for r in targets[gi]]
+    for gi, region in jobs[:64]:
+        fb = amr.grow(fine_mf.ba[gi], NGROW)
+        cb = amr.grow(amr.coarsen(fb, RATIO), 1)
+        crse = rng.random(tuple(cb.extents) + (NCOMP,))
+        fine = np.empty(tuple(fb.extents) + (NCOMP,))
+        ao.interp(crse, np.asarray(cb.as_row()), fine, np.asarray(fb.as_row()), np.asarray(region.as_row()),
+                  [RATIO] * 3, True, 3)
+        done += region.num_pts
+        if time.perf_counter() - t0 > seconds:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": round(done * NCOMP * 8 / dt / 1e9, 3), "unit": "GB/s (interpolated fine bytes)", "cores": 1,
+            "kind": "port", "sample": f"oracle interp (reference amr.py:269-314 arithmetic) on {done} fine cells"}
+
+
+def cpu_sample_restrict(BOX, NGROW, NCOMP, RATIO, seconds=5.0):
+    """cpu_baseline leg of bench_amr.py --op average_down: the numpy oracle of
+    the restriction (reference amr.py:251-264) of one fab."""
+    from oracle import amr_oracle as ao
+    rng = np.random.default_rng(2)
+    fine = rng.random((BOX + 2 * NGROW,) * 3 + (NCOMP,))
+    fb = np.asarray([-NGROW] * 3 + [BOX + NGROW - 1] * 3)
+    vb = np.asarray([0] * 3 + [BOX - 1] * 3)
+    t0 = time.perf_counter()
+    n = 0
+    while time.perf_counter() - t0 < seconds and n < 50:
+        ao.restrict(fine, fb, vb, [RATIO] * 3, 3)
+        n += 1
+    dt = time.perf_counter() - t0
+    return {"value": round(n * BOX ** 3 * NCOMP * 8 / dt / 1e9, 3), "unit": "GB/s (fine bytes restricted)",
+            "cores": 1, "kind": "port", "sample": f"oracle restriction (amr.py:251-264) of one {BOX}^3 fab x{n}"}
+
+
 def cpu_model():
     try:
         with open("/proc/cpuinfo") as f:

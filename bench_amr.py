@@ -28,6 +28,8 @@ import numpy as np
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
+import bench  # noqa: E402  (the CPU-baseline legs live in bench.py)
+
 N_CRSE, BOX, NCOMP, NGROW, RATIO = 256, 64, 4, 2, 2
 PATCH_LO, PATCH_HI = 64, 191  # coarse cells refined
 
@@ -117,7 +119,7 @@ def run(args):
                              "achieved": round(alg / k_mean / 1e9, 1), "peak": hbm,
                              "frac": round(alg / k_mean / 1e9 / hbm, 4), "unit": "GB/s", "peak_source": peak_src,
                              "kernel_ms": round(k_mean * 1e3, 4)})
-        out["cpu_baseline"] = cpu_interp_sample(fine, targets)
+        out["cpu_baseline"] = bench.cpu_sample_interp(fine, targets, NCOMP, NGROW, RATIO)
     else:
         crse_fine = amr.MultiFab(cba, amr.DistributionMapping([0] * len(cba)), NCOMP, 0, cgeom)
         call = lambda: A.average_down(fine, crse_fine, RATIO)  # noqa: E731
@@ -133,7 +135,7 @@ def run(args):
                              "achieved": round(alg / k_mean / 1e9, 1), "peak": hbm,
                              "frac": round(alg / k_mean / 1e9 / hbm, 4), "unit": "GB/s", "peak_source": peak_src,
                              "kernel_ms": round(k_mean * 1e3, 4)})
-        out["cpu_baseline"] = cpu_restrict_sample()
+        out["cpu_baseline"] = bench.cpu_sample_restrict(BOX, NGROW, NCOMP, RATIO)
     if args.op == "heat":
         out.update(heat_bench(args, amr, cdom, cgeom, cba, flush, clean, hbm, peak_src))
     if args.op == "heat2":
@@ -210,45 +212,6 @@ def heat2_bench(args, amr, cdom, cgeom, cba, fba, fgeom, flush, clean):
             "config": {"workload": f"coarse {N_CRSE}^3 periodic / {BOX}^3 boxes + fine patch of {len(fba)} "
                                    f"{BOX}^3 boxes at ratio {RATIO}, ncomp 1, nghost 1, float64",
                        "l2": "flushed before every step (512 MiB write + 256 MiB clean read, outside the events)"}}
-
-
-def cpu_interp_sample(fine_mf, targets, seconds=5.0):
-    """numpy oracle of interp_box (reference arithmetic) on the first regions."""
-    import paper_2403_12179_b200 as amr
-    from oracle import amr_oracle as ao
-    rng = np.random.default_rng(1)
-    t0 = time.perf_counter()
-    done = 0
-    jobs = [(gi, r) for gi in sorted(targets) for r in targets[gi]]
-    for gi, region in jobs[:64]:
-        fb = amr.grow(fine_mf.ba[gi], NGROW)
-        cb = amr.grow(amr.coarsen(fb, RATIO), 1)
-        crse = rng.random(tuple(cb.extents) + (NCOMP,))
-        fine = np.empty(tuple(fb.extents) + (NCOMP,))
-        ao.interp(crse, np.asarray(cb.as_row()), fine, np.asarray(fb.as_row()), np.asarray(region.as_row()),
-                  [RATIO] * 3, True, 3)
-        done += region.num_pts
-        if time.perf_counter() - t0 > seconds:
-            break
-    dt = time.perf_counter() - t0
-    return {"value": round(done * NCOMP * 8 / dt / 1e9, 3), "unit": "GB/s (interpolated fine bytes)", "cores": 1,
-            "kind": "port", "sample": f"oracle interp (reference amr.py:269-314 arithmetic) on {done} fine cells"}
-
-
-def cpu_restrict_sample(seconds=5.0):
-    from oracle import amr_oracle as ao
-    rng = np.random.default_rng(2)
-    fine = rng.random((BOX + 2 * NGROW,) * 3 + (NCOMP,))
-    fb = np.asarray([-NGROW] * 3 + [BOX + NGROW - 1] * 3)
-    vb = np.asarray([0] * 3 + [BOX - 1] * 3)
-    t0 = time.perf_counter()
-    n = 0
-    while time.perf_counter() - t0 < seconds and n < 50:
-        ao.restrict(fine, fb, vb, [RATIO] * 3, 3)
-        n += 1
-    dt = time.perf_counter() - t0
-    return {"value": round(n * BOX ** 3 * NCOMP * 8 / dt / 1e9, 3), "unit": "GB/s (fine bytes restricted)",
-            "cores": 1, "kind": "port", "sample": f"oracle restriction (amr.py:251-264) of one {BOX}^3 fab x{n}"}
 
 
 def main():

@@ -68,6 +68,27 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def traffic_model_min(cfg):
+    """Minimum DRAM bytes of one FillBoundary launch on the uniform periodic
+    layout (scripts/traffic_model.py): 128-B lines holding source cells must
+    be read, 32-B sectors holding ghost cells must be written."""
+    if cfg["kind"] != "fb" or not isinstance(cfg["ngrow"], int):
+        return None
+    b, g = cfg["box"], cfg["ngrow"]
+    n = b + 2 * g
+    idx = np.arange(n)
+    valid = (idx >= g) & (idx < g + b)
+    src1 = valid & ((idx < 2 * g) | (idx >= b))
+    X, Y, Z = np.meshgrid(idx, idx, idx, indexing="ij")
+    isvalid = valid[X] & valid[Y] & valid[Z]
+    src = isvalid & (src1[X] | src1[Y] | src1[Z])
+    off = (X + n * (Y + n * Z)) * 8
+    lines = np.unique(off[src] // 128).size
+    sectors = np.unique(off[~isvalid] // 32).size
+    nfabs = int(np.prod([e // b for e in cfg["ext"]]))
+    return float((lines * 128 + sectors * 32) * cfg["ncomp"] * nfabs)
+
+
 def ncu_traffic(cfg_name):
     p = os.path.join(REPO, "profiles", "ncu_traffic.json")
     try:
@@ -461,6 +482,7 @@ def run_ours(args, cfg, rank, world):
         roof = {"bound": "hbm", "achieved": round(achieved, 2), "peak": hbm_peak, "unit": "GB/s",
                 "frac": round(achieved / hbm_peak, 4),
                 "traffic": ncu_traffic(args.config) if world == 1 else None,
+                "traffic_model_min": traffic_model_min(cfg) if world == 1 else None,
                 "kernel": "ghx_copy_kernel", "algorithmic_bytes_per_launch": int(alg),
                 "peak_source": peak_src, "box_copy_gbs_now": round(best, 1)}
         if world > 1:

@@ -243,7 +243,7 @@ class ClockSampler:
 
 # ----------------------------------------------------------------- CPU leg
 
-def cpu_sample(cfg, seconds=10.0, max_reps=200, workers=None, reps=None, budget=256e6):
+def cpu_sample(cfg, seconds=10.0, max_reps=100000, workers=None, reps=None, budget=256e6):
     """The oracle (numpy restatement of the reference CPU path) on a bounded
     sample of the workload: every segment whose destination is one of the
     first S dst fabs (S = 1/8 of the fabs, capped so a rep moves <= 256 MB),

@@ -182,6 +182,9 @@ __global__ void __launch_bounds__(kAmrThreads, 4) avgdown_kernel(const DevAvgJob
 // 2.5-D blocking: a block is a 32 x 8 (x, y) tile of one job that marches
 // kAdvZ planes in z, carrying u[z-1], u[z], u[z+1] in registers, so each
 // source value comes from HBM once (x/y neighbours hit L1).
+#ifndef GHX_ADV_MINB
+#define GHX_ADV_MINB 4
+#endif
 #ifndef GHX_ADV_PF
 #define GHX_ADV_PF 2
 #endif
@@ -191,7 +194,7 @@ __global__ void __launch_bounds__(kAmrThreads, 4) avgdown_kernel(const DevAvgJob
 constexpr int kAdvTX = 32, kAdvTY = 8, kAdvZ = GHX_ADV_Z, kAdvPF = GHX_ADV_PF;
 
 template <class T, int DIM>
-__global__ void __launch_bounds__(kAmrThreads, 4) advance_kernel(const DevAvgJob *__restrict__ jobs,
+__global__ void __launch_bounds__(kAmrThreads, GHX_ADV_MINB) advance_kernel(const DevAvgJob *__restrict__ jobs,
                                                                  const int4 *__restrict__ btasks, T c0, T c1, T c2) {
   const int4 bt = btasks[blockIdx.x];  // {job, x0 | y0 << 16, z0, nz}
   const DevAvgJob &J = jobs[bt.x];

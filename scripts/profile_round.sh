@@ -8,7 +8,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/prof/launches_C2.csv python bench.py --config C2 --steps 5 --warmup 3 --no-e2e --no-cpu \
   > gpurun_out/prof/launches_C2.log 2>&1
 echo "launch list rc=$?"
-for c in C2 C3; do
+for c in C2 C3 C5; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:ghx_copy_kernel -s 4 -c 1 -f \
     -o gpurun_out/prof/full_$c python bench.py --config $c --steps 3 --warmup 3 --no-e2e --no-cpu \
     > gpurun_out/prof/full_$c.log 2>&1

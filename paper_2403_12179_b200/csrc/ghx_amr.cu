@@ -32,6 +32,13 @@ using ghx::set_error;
 namespace {
 
 constexpr int kAmrThreads = 256;
+#ifndef GHX_INTERP_MINB
+#define GHX_INTERP_MINB 5
+#endif
+#ifndef GHX_INTERP_COMPS
+#define GHX_INTERP_COMPS 2
+#endif
+constexpr int kInterpComps = GHX_INTERP_COMPS;  // interp: components whose loads are batched
 
 struct Geo3 {
   int64_t lo[3], n[3];  // storage box lo, extents
@@ -65,14 +72,14 @@ __device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, 
 __device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
 __device__ __forceinline__ float div_rn(float a, float b) { return __fdiv_rn(a, b); }
 
-// One thread per fine cell of the launch (x fastest: coalesced fine stores),
-// all components.  LINEAR, per axis d < spacedim in order (amr.py:302-313):
+// One thread per fine cell: blocks take kAmrThreads consecutive cells of one
+// job (x fastest: coalesced fine stores), all components.  LINEAR, per axis d < spacedim in order (amr.py:302-313):
 //   slope = 0.5 * (c[p+e_d] - c[p-e_d])          (storage type T)
 //   off   = ((f mod r) + 0.5) / r - 0.5          (float64)
 //   v     = T(double(v) + double(slope) * off)   (numpy's float64 loop for
 //                                                 v += slope * off)
 template <class T, bool LINEAR>
-__global__ void __launch_bounds__(kAmrThreads, 3) interp_kernel(const DevInterpJob *__restrict__ jobs,
+__global__ void __launch_bounds__(kAmrThreads, GHX_INTERP_MINB) interp_kernel(const DevInterpJob *__restrict__ jobs,
                                                              const int4 *__restrict__ btasks, int ncomp, int r0,
                                                              int r1, int r2, int spacedim) {
   const int r[3] = {r0, r1, r2};
@@ -103,24 +110,37 @@ __global__ void __launch_bounds__(kAmrThreads, 3) interp_kernel(const DevInterpJ
     const T *crse = reinterpret_cast<const T *>(J.crse);
     T *fine = reinterpret_cast<T *>(J.fine);
     const int64_t step[3] = {1, csy, csz};
-    for (int c = 0; c < ncomp; ++c) {
-      const T *cc = crse + co + c * csc;
-      // every coarse value this cell needs is requested before the arithmetic
-      T v = __ldg(cc), up[3], dn[3];
-      if (LINEAR) {
+    // components in groups of kInterpComps: every coarse value of a group is
+    // requested before any arithmetic (up to 7 * kInterpComps loads in flight)
+    for (int c0 = 0; c0 < ncomp; c0 += kInterpComps) {
+      T v[kInterpComps], up[kInterpComps][3], dn[kInterpComps][3];
 #pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          up[d] = d < spacedim ? __ldg(cc + step[d]) : T(0);
-          dn[d] = d < spacedim ? __ldg(cc - step[d]) : T(0);
-        }
+      for (int i = 0; i < kInterpComps; ++i) {
+        if (c0 + i >= ncomp) break;
+        const T *cc = crse + co + (c0 + i) * csc;
+        v[i] = __ldg(cc);
+        if (LINEAR) {
 #pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          if (d >= spacedim) break;
-          const T slope = mul_rn(T(0.5), sub_rn(up[d], dn[d]));
-          v = T(__dadd_rn((double)v, __dmul_rn((double)slope, off[d])));
+          for (int d = 0; d < 3; ++d) {
+            up[i][d] = d < spacedim ? __ldg(cc + step[d]) : T(0);
+            dn[i][d] = d < spacedim ? __ldg(cc - step[d]) : T(0);
+          }
         }
       }
-      fine[fo + c * fsc] = v;
+#pragma unroll
+      for (int i = 0; i < kInterpComps; ++i) {
+        if (c0 + i >= ncomp) break;
+        T w = v[i];
+        if (LINEAR) {
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            if (d >= spacedim) break;
+            const T slope = mul_rn(T(0.5), sub_rn(up[i][d], dn[i][d]));
+            w = T(__dadd_rn((double)w, __dmul_rn((double)slope, off[d])));
+          }
+        }
+        fine[fo + (c0 + i) * fsc] = w;
+      }
     }
   }
 }
@@ -311,8 +331,9 @@ namespace {
 
 constexpr int kCellsPerBlock = kAmrThreads * 4;
 
-// Block tasks: interp / average_down blocks take kCellsPerBlock consecutive
-// cells of one job; the stencil takes 32 x 8 x kAdvZ tiles of one job.
+// Block tasks: interp blocks take kAmrThreads consecutive cells of one job
+// (one per thread), average_down blocks kCellsPerBlock; the stencil takes
+// 32 x 8 x kAdvZ tiles of one job.
 template <class J>
 std::vector<int4> block_tasks(const ghx_xfer *x, const std::vector<J> &jobs) {
   std::vector<int4> t;
@@ -325,8 +346,9 @@ std::vector<int4> block_tasks(const ghx_xfer *x, const std::vector<J> &jobs) {
             t.push_back(make_int4((int)j, (int)(x0 | (y0 << 16)), (int)z0, (int)std::min<int64_t>(kAdvZ, d.rn[2] - z0)));
     } else {
       const int64_t cells = d.rn[0] * d.rn[1] * d.rn[2];
-      for (int64_t c0 = 0; c0 < cells; c0 += kCellsPerBlock)
-        t.push_back(make_int4((int)j, (int)c0, (int)std::min<int64_t>(kCellsPerBlock, cells - c0), 0));
+      const int64_t per = x->kind == 0 ? kAmrThreads : kCellsPerBlock;  // interp: one cell per thread
+      for (int64_t c0 = 0; c0 < cells; c0 += per)
+        t.push_back(make_int4((int)j, (int)c0, (int)std::min<int64_t>(per, cells - c0), 0));
     }
   }
   return t;
@@ -361,19 +383,20 @@ int xfer_launch(const ghx_xfer *x, cudaStream_t st) {
   if (x->kind == 0) {
     const DevInterpJob *p = static_cast<const DevInterpJob *>(x->djobs);
     const bool lin = x->scheme == GHX_INTERP_LINEAR;
+    const int g = x->blocks;
     if (x->elem_bytes == 8) {
       if (lin)
-        interp_kernel<double, true><<<x->blocks, kAmrThreads, 0, st>>>(p, x->dtasks, x->ncomp, x->r[0], x->r[1],
+        interp_kernel<double, true><<<g, kAmrThreads, 0, st>>>(p, x->dtasks, x->ncomp, x->r[0], x->r[1],
                                                                        x->r[2], x->spacedim);
       else
-        interp_kernel<double, false><<<x->blocks, kAmrThreads, 0, st>>>(p, x->dtasks, x->ncomp, x->r[0], x->r[1],
+        interp_kernel<double, false><<<g, kAmrThreads, 0, st>>>(p, x->dtasks, x->ncomp, x->r[0], x->r[1],
                                                                         x->r[2], x->spacedim);
     } else {
       if (lin)
-        interp_kernel<float, true><<<x->blocks, kAmrThreads, 0, st>>>(p, x->dtasks, x->ncomp, x->r[0], x->r[1],
+        interp_kernel<float, true><<<g, kAmrThreads, 0, st>>>(p, x->dtasks, x->ncomp, x->r[0], x->r[1],
                                                                       x->r[2], x->spacedim);
       else
-        interp_kernel<float, false><<<x->blocks, kAmrThreads, 0, st>>>(p, x->dtasks, x->ncomp, x->r[0], x->r[1],
+        interp_kernel<float, false><<<g, kAmrThreads, 0, st>>>(p, x->dtasks, x->ncomp, x->r[0], x->r[1],
                                                                        x->r[2], x->spacedim);
     }
   } else if (x->kind == 2 || x->kind == 3) {

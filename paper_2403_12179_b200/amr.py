@@ -12,6 +12,7 @@ launch per call for all fabs (the reference's ``fused_segments``).
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 
@@ -250,10 +251,6 @@ def fill_patch(fine: MultiFab, coarse: MultiFab, fine_geom: Geometry, coarse_geo
     rank the three steps are enqueued back to back on the current stream and
     the host waits once at the end."""
     serial = comm.current_ctx().nranks == 1
-    if serial:
-        comm.prepare_fill_boundary(fine, fine_geom).enqueue(_stream(fine.device))
-    else:
-        comm.fill_boundary(fine, fine_geom, backend=backend)
     reach = 1 if scheme == LINEAR else 0
     key = comm.PlanKey(coarse.ba.uid, coarse.dm.uid, fine.ba.uid, fine.dm.uid, (reach,) * len(fine.ngrow),
                        fine.ngrow.comps, fine.ba.ixtype.flags, fine_geom.periodic, "fill_patch")
@@ -270,17 +267,66 @@ def fill_patch(fine: MultiFab, coarse: MultiFab, fine_geom: Geometry, coarse_geo
         fine.plan_cache[key] = cached
         fine.plan_builds += 1
     targets, gather_list, dst_ranks, plan = cached
+    if not serial:
+        comm.fill_boundary(fine, fine_geom, backend=backend)
+        if not targets:
+            return
+        owned = comm.gather_targets(plan, gather_list, dst_ranks, coarse)
+        comm.gather_fabs(gather_list, dst_ranks, owned, coarse, coarse_geom, backend=backend, plan=plan)
+        _interp_xfer(fine, coarse, key, targets, owned, ratio, scheme).run()
+        _sync(fine.device)
+        return
+    fb = comm.prepare_fill_boundary(fine, fine_geom)
     if not targets:
-        if serial and _wait:
+        fb.enqueue(_stream(fine.device))
+        if _wait:
             _sync(fine.device)
         return
     owned = comm.gather_targets(plan, gather_list, dst_ranks, coarse)
-    if serial:
-        if not plan.is_empty:
-            comm.exchange_for(plan, coarse, comm._gather_set(plan, gather_list, dst_ranks, coarse), 0, 0,
-                              coarse.ncomp).enqueue(_stream(fine.device))
+    gather = None if plan.is_empty else comm.exchange_for(
+        plan, coarse, comm._gather_set(plan, gather_list, dst_ranks, coarse), 0, 0, coarse.ncomp)
+    xf = _interp_xfer(fine, coarse, key, targets, owned, ratio, scheme)
+    # Single rank: the FillBoundary writes the covered ghost cells, the
+    # gather + interp the uncovered ones (disjoint by construction, and the
+    # interp reads only the gathered coarse data), so they run on two
+    # streams, forked from and joined back to the current one.
+    import torch
+    main = torch.cuda.current_stream(fine.device)
+    if _fp_overlap():
+        side = _side_stream(fine.device)
+        side.wait_stream(main)
+        fb.enqueue(main.cuda_stream)
+        with torch.cuda.stream(side):
+            if gather is not None:
+                gather.enqueue(side.cuda_stream)
+            xf.run()
+        main.wait_stream(side)
     else:
-        comm.gather_fabs(gather_list, dst_ranks, owned, coarse, coarse_geom, backend=backend, plan=plan)
+        fb.enqueue(main.cuda_stream)
+        if gather is not None:
+            gather.enqueue(main.cuda_stream)
+        xf.run()
+    if _wait:
+        _sync(fine.device)
+
+
+_side_streams: dict = {}
+
+
+def _side_stream(device: int):
+    import torch
+    st = _side_streams.get(device)
+    if st is None:
+        st = _side_streams[device] = torch.cuda.Stream(device)
+    return st
+
+
+def _fp_overlap() -> bool:
+    return os.environ.get("GHX_FP_OVERLAP", "1") != "0"
+
+
+def _interp_xfer(fine: MultiFab, coarse: MultiFab, key, targets, owned, ratio: int, scheme: str) -> _Xfer:
+    """The prepared interp launch of a fill_patch plan (validated once)."""
     xkey = ("fill_patch_interp", key, int(ratio), scheme, fine.ncomp)
     xf = fine._peer_cache.get(xkey)
     if xf is None:
@@ -299,6 +345,4 @@ def fill_patch(fine: MultiFab, coarse: MultiFab, fine_geom: Geometry, coarse_geo
             raise ValueError(f"unknown interpolation scheme {scheme!r}")
         xf = fine._peer_cache[xkey] = _prepare_interp(jobs, fine.ncomp, int(ratio), scheme, fine.dtype.itemsize,
                                                       fine.device)
-    xf.run()
-    if _wait or not serial:
-        _sync(fine.device)
+    return xf

@@ -17,6 +17,7 @@ tagging, the Gaussian oracle, integrals, plotfiles).
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 
@@ -111,8 +112,23 @@ def _enqueue_step(levels: list, geoms: list, dt: float, diffusivity: float, ref_
     host wait (also what HeatLoop captures into a CUDA graph)."""
     import torch
     dev = levels[0][0].device
-    st = torch.cuda.current_stream(dev).cuda_stream
-    comm.prepare_fill_boundary(levels[0][0], geoms[0]).enqueue(st)
+    main = torch.cuda.current_stream(dev)
+    if len(levels) > 1 and os.environ.get("GHX_LEVEL_OVERLAP", "1") != "0":
+        # The coarse chain (FillBoundary, stencil into unew) and the fine one
+        # (fill_patch -- its gather reads coarse VALID cells only, which
+        # neither coarse kernel writes -- then the fine stencil) are
+        # independent; average_down writes coarse unew, so it joins both.
+        lvl = _level_stream(dev)
+        lvl.wait_stream(main)
+        comm.prepare_fill_boundary(levels[0][0], geoms[0]).enqueue(main.cuda_stream)
+        _stencil(levels[0][0], levels[0][1], dt, diffusivity, geoms[0], "all").run()
+        with torch.cuda.stream(lvl):
+            fill_patch(levels[1][0], levels[0][0], geoms[1], geoms[0], ref_ratio, LINEAR, _wait=False)
+            _stencil(levels[1][0], levels[1][1], dt, diffusivity, geoms[1], "all").run()
+        main.wait_stream(lvl)
+        average_down(levels[1][1], levels[0][1], ref_ratio, _wait=False)
+        return [(w, u) for (u, w) in levels]
+    comm.prepare_fill_boundary(levels[0][0], geoms[0]).enqueue(main.cuda_stream)
     if len(levels) > 1:
         fill_patch(levels[1][0], levels[0][0], geoms[1], geoms[0], ref_ratio, LINEAR, _wait=False)
     for lv, (u, w) in enumerate(levels):
@@ -120,6 +136,17 @@ def _enqueue_step(levels: list, geoms: list, dt: float, diffusivity: float, ref_
     if len(levels) > 1:
         average_down(levels[1][1], levels[0][1], ref_ratio, _wait=False)
     return [(w, u) for (u, w) in levels]
+
+
+_level_streams: dict = {}
+
+
+def _level_stream(device: int):
+    import torch
+    st = _level_streams.get(device)
+    if st is None:
+        st = _level_streams[device] = torch.cuda.Stream(device)
+    return st
 
 
 def heat_step(levels: list, geoms: list, dt: float, diffusivity: float, ref_ratio: int = 2, backend=None,

@@ -40,6 +40,8 @@ timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,launch__registers_per_thread,sm__warps_active.avg.pct_of_peak_sustained_active \
   --clock-control none --csv -k regex:"advance_kernel" -c 2 python bench_amr.py --op heat --steps 3 --warmup 3 \
   > gpurun_out/prof/traffic_advance.csv 2> gpurun_out/prof/traffic_advance.err
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"advance_kernel" -c 1 -f \
+  -o gpurun_out/prof/full_advance python bench_amr.py --op heat --steps 3 --warmup 3 > gpurun_out/prof/full_advance.log 2>&1
 echo "amr ncu done"
 # microbenchmarks behind the roofline discussion
 (cd scripts/microbench && nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/seam_probe seam_probe.cu \

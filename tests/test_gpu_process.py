@@ -84,8 +84,20 @@ CASES = [("C1", 64, 32, 1, 1, "C1_x2", {"GHX_REMOTE": "direct"}), ("C3", 512, 12
 @pytest.mark.parametrize("cfg", CASES, ids=["C1-ipc-direct", "C3-ipc-packed", "C3-ipc-direct", "C1-devbarrier-packed",
                                             "C1-fallback", "C3-fallback", "C1-arena-ipc"])
 def test_two_processes_one_gpu(cfg):
+    _run(cfg, 2)
+
+
+# C3 at 4 and 8 ranks (8 and 40 ordered pairs): every rank maps
+# every peer it pushes to; message accounting against the reference's plan
+@pytest.mark.parametrize("world,env", [(4, {}), (4, {"GHX_TRANSPORT": "nccl"}), (8, {}),
+                                       (4, {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "30"})],
+                         ids=["C3x4-ipc-packed", "C3x4-fallback", "C3x8-ipc-packed", "C3x4-devbarrier"])
+def test_many_processes_one_gpu(world, env):
+    _run(("C3", 512, 128, 8, 2, f"C3_x{world}", env), world)
+
+
+def _run(cfg, world):
     name, n, b, nc, ng, golden, env = cfg
-    world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()

@@ -158,7 +158,8 @@ def heat_step(levels: list, geoms: list, dt: float, diffusivity: float, ref_rati
     which is returned.  With ``overlap`` the interior stencils run on a side
     stream during the exchanges.  Measured on one B200 (bench_amr.py --op
     heat): off by default -- with the exchange local, both phases are
-    HBM-bound and the split only adds a launch (0.156 vs 0.170 ms); it is
+    HBM-bound and the split adds a launch and a one-cell shell pass whose
+    x-faces are isolated seams again (0.103 vs 0.122 ms); it is
     meant for exchanges whose latency is remote (NVLink / host memory)."""
     import torch
     if not 1 <= len(levels) <= 2:

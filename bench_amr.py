@@ -126,10 +126,13 @@ def run(args):
         t_mean, t_min = timed(call, args.steps, args.warmup, flush, clean)
         fine_cells = sum(b.num_pts for b in fba)
         crse_cells = fine_cells // RATIO ** 3
-        xf = [v for k, v in fine._peer_cache.items() if isinstance(k, tuple) and k[0] == "average_down_xfer"][0]
+        xf = [v for k, v in fine._peer_cache.items()
+              if isinstance(k, tuple) and k[0] in ("average_down_xfer", "average_down_direct")][0]
         k_mean, _ = timed(xf.run, args.steps, args.warmup, flush, clean)
         alg = (fine_cells + crse_cells) * NCOMP * item
         out.update(metric="average_down GB/s (fine bytes restricted, restriction + ParallelCopy)",
+                   path="direct restriction into the coarse fabs (single rank)"
+                   if os.environ.get("GHX_AVGDOWN_DIRECT", "1") != "0" else "restriction into tmp + ParallelCopy",
                    value=round(fine_cells * NCOMP * item / t_mean / 1e9, 2), ms_per_step=round(t_mean * 1e3, 4),
                    roofline={"kernel": "avgdown_kernel<double>", "bound": "hbm", "algorithmic_bytes_per_launch": alg,
                              "achieved": round(alg / k_mean / 1e9, 1), "peak": hbm,

@@ -158,6 +158,11 @@ def average_down(fine: MultiFab, coarse: MultiFab, ratio: int, backend=None, *, 
     if fine.ncomp != coarse.ncomp:
         raise ValueError("component count mismatch")
     tmp = _restriction_layout(fine, ratio)
+    if comm.current_ctx().nranks == 1 and os.environ.get("GHX_AVGDOWN_DIRECT", "1") != "0":
+        _average_down_direct(fine, coarse, tmp, ratio)
+        if _wait:
+            _sync(fine.device)
+        return
     key = ("average_down_xfer", fine.ba.uid, fine.dm.uid, ratio, fine.ncomp, fine.dtype.str)
     xf = fine._peer_cache.get(key)
     if xf is None:
@@ -181,6 +186,38 @@ def average_down(fine: MultiFab, coarse: MultiFab, ratio: int, backend=None, *, 
             _sync(fine.device)
     else:
         comm.parallel_copy(coarse, tmp, backend=backend)
+
+
+def _average_down_direct(fine: MultiFab, coarse: MultiFab, tmp: MultiFab, ratio: int) -> None:
+    """Single rank: restrict straight into the coarse fabs.  The
+    ParallelCopy tmp -> coarse (amr.py:265) is planned as the reference
+    does (cached on ``coarse``, ``plan_builds`` as in the reference); its
+    segments -- pieces of coarsened fine boxes inside coarse boxes, no
+    shift -- become the restriction jobs, so the kernel writes exactly the
+    cells the copy would, with the same bits, and tmp is never touched."""
+    ncomp, gs, gd = comm._pc_args(coarse, tmp, 0, 0, None, 0, 0)
+    plan = comm._parallel_copy_plan(coarse, tmp, gs, gd, None)
+    if plan.is_empty:
+        return
+    key = ("average_down_direct", plan.uid, coarse.uid, ratio, fine.ncomp, fine.dtype.str)
+    xf = fine._peer_cache.get(key)
+    if xf is None:
+        segs = plan.local_by_rank.get(0, [])
+        rows = np.zeros((len(segs), N.JOB_WORDS), np.int64)
+        for n, sg in enumerate(segs):
+            assert not any(sg.shift) and sg.src_box == sg.dst_box
+            ff, cf = fine.fabs[sg.src_fab], coarse.fabs[sg.dst_fab]
+            rows[n, 0] = np.uint64(ff.ptr).view(np.int64)
+            rows[n, 1:7] = _row(ff.box)
+            rows[n, 7] = np.uint64(cf.ptr).view(np.int64)
+            rows[n, 8:14] = _row(cf.box)
+            rows[n, 14:20] = _row(sg.dst_box)
+        h = C.c_void_p()
+        N.check(N.lib.ghx_average_down_prepare(C.c_void_p(rows.ctypes.data), len(rows), fine.ncomp,
+                                               N.i32p(_ratio3(ratio)), config.spacedim, fine.dtype.itemsize,
+                                               fine.device, C.byref(h)))
+        xf = fine._peer_cache[key] = _Xfer(h.value, fine.device)
+    xf.run()
 
 
 # ---------------------------------------------------------------- fill_patch

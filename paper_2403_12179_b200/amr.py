@@ -320,8 +320,13 @@ def fill_patch(fine: MultiFab, coarse: MultiFab, fine_geom: Geometry, coarse_geo
             _sync(fine.device)
         return
     owned = comm.gather_targets(plan, gather_list, dst_ranks, coarse)
-    gather = None if plan.is_empty else comm.exchange_for(
-        plan, coarse, comm._gather_set(plan, gather_list, dst_ranks, coarse), 0, 0, coarse.ncomp)
+    gather = None
+    if not plan.is_empty:
+        if os.environ.get("GHX_FP_GATHER", "regions") == "regions":
+            gather = _region_gather(fine, coarse, coarse_geom, key, targets, owned, ratio, reach)
+        else:
+            gather = comm.exchange_for(plan, coarse, comm._gather_set(plan, gather_list, dst_ranks, coarse), 0, 0,
+                                       coarse.ncomp)
     xf = _interp_xfer(fine, coarse, key, targets, owned, ratio, scheme)
     # Single rank: the FillBoundary writes the covered ghost cells, the
     # gather + interp the uncovered ones (disjoint by construction, and the
@@ -345,6 +350,50 @@ def fill_patch(fine: MultiFab, coarse: MultiFab, fine_geom: Geometry, coarse_geo
         xf.run()
     if _wait:
         _sync(fine.device)
+
+
+class _RegionSet:
+    """Destination of the single-rank fill_patch gather: one slot per coarse
+    box the interpolation reads (a region's coarsened footprint, grown by the
+    stencil reach), addressed inside its parent gather-target fab.  The
+    reference gathers each target's whole box (comm.py:432-462); only these
+    cells are ever read, so the fine result is the same while the gather
+    moves the thin shells instead of whole coarsened fabs."""
+
+    def __init__(self, parents: dict, slots: list, like: MultiFab):
+        from .mesh import _next_uid
+        self.ncomp, self.dtype, self.device = like.ncomp, like.dtype, like.device
+        self.ngrow = IntVect(*([0] * len(like.ngrow)))
+        self.uid = _next_uid()
+        self._peer_cache: dict = {}
+        self._parents = parents  # the target fabs (and their slab) stay alive with the set
+        self.local_indices = tuple(range(len(slots)))
+        self._rows = np.ascontiguousarray(
+            np.asarray([parents[fid].box.as_row() for fid, _ in slots], np.int64).reshape(-1, 6))
+        self._ptrs = np.array([parents[fid].ptr for fid, _ in slots], np.uint64)
+
+    def storage_rows(self) -> np.ndarray:
+        return self._rows
+
+
+def _region_gather(fine: MultiFab, coarse: MultiFab, coarse_geom: Geometry, key, targets: dict, owned: dict,
+                   ratio: int, reach: int) -> "comm.Exchange":
+    gkey = ("fill_patch_region_gather", key, coarse.uid, coarse.ncomp)
+    ex = fine._peer_cache.get(gkey)
+    if ex is None:
+        slots = []
+        for gi in sorted(targets):
+            seen = set()
+            for r in targets[gi]:
+                need = grow(coarsen(r, int(ratio)), reach)
+                if tuple(need.as_row()) not in seen:
+                    seen.add(tuple(need.as_row()))
+                    slots.append((gi, need))
+        plan = comm.build_gather_plan(list(enumerate(b for _, b in slots)), [0] * len(slots), coarse, coarse_geom)
+        dst = _RegionSet(owned, slots, coarse)
+        ex = fine._peer_cache[gkey] = (plan, dst, None if plan.is_empty else
+                                       comm.exchange_for(plan, coarse, dst, 0, 0, coarse.ncomp))
+    return ex[2]
 
 
 _side_streams: dict = {}

@@ -199,9 +199,11 @@ __global__ void __launch_bounds__(kAmrThreads, 4) avgdown_kernel(const DevAvgJob
 // One heat-equation step (reference heat.py:172-189, comp 0):
 //   acc = u;  acc += c_d * ((u[+e_d] - 2*u) + u[-e_d])   for d < DIM
 // in numpy's order, storage type T throughout (coefficients rounded to T).
-// 2.5-D blocking: a block is a 32 x 8 (x, y) tile of one job that marches
-// kAdvZ planes in z, carrying u[z-1], u[z], u[z+1] in registers, so each
-// source value comes from HBM once (x/y neighbours hit L1).
+// 2.5-D blocking: a block is a TX x (256 / TX) (x, y) tile of one job that
+// marches kAdvZ planes in z, carrying u[z-1], u[z], u[z+1] in registers, so
+// each source value comes from HBM once (x/y neighbours hit L1).  TX = 64
+// (longer contiguous runs per plane) when the regions are wide enough to
+// keep the lanes busy, else 32.
 #ifndef GHX_ADV_MINB
 #define GHX_ADV_MINB 4
 #endif
@@ -209,16 +211,16 @@ __global__ void __launch_bounds__(kAmrThreads, 4) avgdown_kernel(const DevAvgJob
 #define GHX_ADV_PF 2
 #endif
 #ifndef GHX_ADV_Z
-#define GHX_ADV_Z 16
+#define GHX_ADV_Z 32
 #endif
-constexpr int kAdvTX = 32, kAdvTY = 8, kAdvZ = GHX_ADV_Z, kAdvPF = GHX_ADV_PF;
+constexpr int kAdvZ = GHX_ADV_Z, kAdvPF = GHX_ADV_PF;
 
-template <class T, int DIM>
+template <class T, int DIM, int TX>
 __global__ void __launch_bounds__(kAmrThreads, GHX_ADV_MINB) advance_kernel(const DevAvgJob *__restrict__ jobs,
                                                                  const int4 *__restrict__ btasks, T c0, T c1, T c2) {
   const int4 bt = btasks[blockIdx.x];  // {job, x0 | y0 << 16, z0, nz}
   const DevAvgJob &J = jobs[bt.x];
-  const int tx = threadIdx.x & (kAdvTX - 1), ty = threadIdx.x / kAdvTX;
+  const int tx = threadIdx.x & (TX - 1), ty = threadIdx.x / TX;
   const int64_t xr = (bt.y & 0xffff) + tx, yr = (bt.y >> 16) + ty;
   if (xr >= J.rn[0] || yr >= J.rn[1]) return;
   const int64_t x = J.rlo[0] + xr, y = J.rlo[1] + yr, z = J.rlo[2] + bt.z;
@@ -325,6 +327,7 @@ struct ghx_xfer {
   int64_t rpow = 1;
   double coef[3] = {0, 0, 0};  // advance: dt * diffusivity / dx_d^2
   int blocks = 0;
+  int tile_x = 32;  // advance: x extent of a block tile (32 or 64)
 };
 
 namespace {
@@ -333,16 +336,25 @@ constexpr int kCellsPerBlock = kAmrThreads * 4;
 
 // Block tasks: interp blocks take kAmrThreads consecutive cells of one job
 // (one per thread), average_down blocks kCellsPerBlock; the stencil takes
-// 32 x 8 x kAdvZ tiles of one job.
+// TX x (256 / TX) x kAdvZ tiles of one job.
 template <class J>
-std::vector<int4> block_tasks(const ghx_xfer *x, const std::vector<J> &jobs) {
+std::vector<int4> block_tasks(ghx_xfer *x, const std::vector<J> &jobs) {
   std::vector<int4> t;
+  if (x->kind == 2) {  // 64-wide tiles when they waste <= 1/4 of the lanes over the launch
+    int64_t cells = 0, lanes64 = 0;
+    for (const J &d : jobs) {
+      cells += d.rn[0] * d.rn[1] * d.rn[2];
+      lanes64 += (d.rn[0] + 63) / 64 * 64 * d.rn[1] * d.rn[2];
+    }
+    x->tile_x = (cells > 0 && 4 * cells >= 3 * lanes64) ? 64 : 32;
+  }
+  const int tx = x->tile_x, ty = kAmrThreads / tx;
   for (size_t j = 0; j < jobs.size(); ++j) {
     const J &d = jobs[j];
-    if (x->kind == 2) {  // 32 x 8 x kAdvZ tiles
+    if (x->kind == 2) {
       for (int64_t z0 = 0; z0 < d.rn[2]; z0 += kAdvZ)
-        for (int64_t y0 = 0; y0 < d.rn[1]; y0 += kAdvTY)
-          for (int64_t x0 = 0; x0 < d.rn[0]; x0 += kAdvTX)
+        for (int64_t y0 = 0; y0 < d.rn[1]; y0 += ty)
+          for (int64_t x0 = 0; x0 < d.rn[0]; x0 += tx)
             t.push_back(make_int4((int)j, (int)(x0 | (y0 << 16)), (int)z0, (int)std::min<int64_t>(kAdvZ, d.rn[2] - z0)));
     } else {
       const int64_t cells = d.rn[0] * d.rn[1] * d.rn[2];
@@ -403,8 +415,10 @@ int xfer_launch(const ghx_xfer *x, cudaStream_t st) {
     const DevAvgJob *p = static_cast<const DevAvgJob *>(x->djobs);
     const double *c = x->coef;
 #define GHX_ADV(T, D)                                                                                        \
-  if (x->kind == 2)                                                                                          \
-    advance_kernel<T, D><<<x->blocks, kAmrThreads, 0, st>>>(p, x->dtasks, (T)c[0], (T)c[1], (T)c[2]);        \
+  if (x->kind == 2 && x->tile_x == 64)                                                                       \
+    advance_kernel<T, D, 64><<<x->blocks, kAmrThreads, 0, st>>>(p, x->dtasks, (T)c[0], (T)c[1], (T)c[2]);    \
+  else if (x->kind == 2)                                                                                     \
+    advance_kernel<T, D, 32><<<x->blocks, kAmrThreads, 0, st>>>(p, x->dtasks, (T)c[0], (T)c[1], (T)c[2]);    \
   else                                                                                                       \
     advance_flat_kernel<T, D><<<x->blocks, kAmrThreads, 0, st>>>(p, x->dtasks, (T)c[0], (T)c[1], (T)c[2])
     if (x->elem_bytes == 8) {

@@ -240,3 +240,36 @@ def test_heat_loop_rank_invariant():
         assert got.keys() == base.keys()
         for k in base:
             assert np.array_equal(got[k], base[k]), (n, k)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("ext,dt", [((70, 13, 40), np.float64), ((128, 9, 33), np.float32),
+                                    ((20, 17, 35), np.float64), ((96, 5, 3), np.float64)])
+def test_advance_tiles_match_oracle(ext, dt):
+    """The stencil's tilings (64-wide tiles for wide regions, 32-wide
+    otherwise; partial x / y tiles; z split into 32-plane tasks) against the
+    oracle restatement of heat.py:172-189, raw bits, ghosts from the hash."""
+    import paper_2403_12179_b200 as amr
+    from paper_2403_12179_b200 import heat as H
+    from gpu_util import bits_of, upload
+    from oracle import amr_oracle as ao
+    from oracle import inputs
+    amr.config.set_spacedim(3)
+    amr.config.set_real_dtype(dt)
+    dom = amr.Box((0, 0, 0), tuple(e - 1 for e in ext))
+    geom = amr.Geometry(dom, (0.0,) * 3, (1.0,) * 3, (True,) * 3)
+    ba = amr.BoxArray([dom])
+    dm = amr.DistributionMapping([0])
+    u = amr.MultiFab(ba, dm, 1, 1, geom)
+    w = amr.MultiFab(ba, dm, 1, 1, geom)
+    g = [-1, -1, -1, ext[0], ext[1], ext[2]]
+    host = inputs.make_fab(g[:3], g[3:], 1, dt, g[:3], g[3:], [-1] * 3, [e for e in ext])  # every cell hashed
+    upload(u.fabs[0], host)
+    w.setval(0.0)
+    dt_, kappa = 1e-4, 1.0
+    H.advance_level(u, w, dt_, kappa, geom)
+    new = ao.advance(host, g, [0, 0, 0, *[e - 1 for e in ext]], H._coefs(dt_, kappa, geom), 3)
+    full = np.zeros_like(host)
+    full[1:-1, 1:-1, 1:-1, 0] = new
+    exp = inputs.bits(full).ravel(order="F")
+    assert np.array_equal(bits_of(w.fabs[0]), exp)

@@ -8,7 +8,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/prof/launches_C2.csv python bench.py --config C2 --steps 5 --warmup 3 --no-e2e --no-cpu \
   > gpurun_out/prof/launches_C2.log 2>&1
 echo "launch list rc=$?"
-for c in C2 C3 C5; do
+for c in C2 C3 C4 C5; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:ghx_copy_kernel -s 4 -c 1 -f \
     -o gpurun_out/prof/full_$c python bench.py --config $c --steps 3 --warmup 3 --no-e2e --no-cpu \
     > gpurun_out/prof/full_$c.log 2>&1
@@ -42,6 +42,9 @@ timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
   > gpurun_out/prof/traffic_advance.csv 2> gpurun_out/prof/traffic_advance.err
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"advance_kernel" -c 1 -f \
   -o gpurun_out/prof/full_advance python bench_amr.py --op heat --steps 3 --warmup 3 > gpurun_out/prof/full_advance.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file gpurun_out/prof/launches_fill_patch.csv python bench_amr.py --op fill_patch --steps 3 --warmup 3 \
+  > gpurun_out/prof/launches_fill_patch.log 2>&1
 echo "amr ncu done"
 # microbenchmarks behind the roofline discussion
 (cd scripts/microbench && nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/seam_probe seam_probe.cu \

@@ -49,7 +49,7 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread", "launch__grid_size",
         "launch__block_size", "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
         "sm__throughput.avg.pct_of_peak_sustained_elapsed"]
-for c in ["C2", "C3", "C5", "advance"]:
+for c in ["C2", "C3", "C4", "C5", "advance"]:
     rep = f"{src}/full_{c}.ncu-rep"
     if not os.path.exists(rep):
         continue

@@ -583,9 +583,24 @@ def e2e_leg(args, amr, cfg, L, world, ghost_bytes, x):
         ts.append(float(dt.item()))
     t = statistics.median(ts)
     h2d = sum(h.numel() * h.element_size() for h in host)
+    verified = None
+    if cfg["kind"] == "fb" and mf.local_indices and host:
+        # the D2H'd result of this rank's first fab, checked like the device one
+        import ctypes as C
+        from paper_2403_12179_b200 import _native as N
+        f = mf.fabs[mf.local_indices[0]]
+        raw = f.raw()
+        off = (raw.data_ptr() - tensors[0].data_ptr()) // raw.element_size()
+        exp = torch.empty(raw.numel(), dtype=torch.int64, device=raw.device)
+        N.check(N.lib.ghx_fill_hash_wrapped(
+            C.c_void_p(exp.data_ptr()), N.i64p(np.asarray(f.box.as_row(), np.int64)), mf.ncomp,
+            N.i64p(np.asarray(L["dom"].as_row(), np.int64)), N.i32p(np.ones(3, np.int32)),
+            C.c_uint64(SEED), 8, None))
+        got = host[0].view(torch.int64)[off:off + raw.numel()]
+        verified = bool(torch.equal(got, exp.cpu()))
     return {"value": round(ghost_bytes / t / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(host[0].numel() * host[0].element_size()) if host else 0,
-            "ms_per_step": round(t * 1e3, 3), "steps": steps,
+            "ms_per_step": round(t * 1e3, 3), "steps": steps, "verified": verified,
             "path": "pinned host copy of each rank's fab storage -> H2D -> public API exchange -> D2H"}
 
 

@@ -584,6 +584,10 @@ def _transport() -> str:
     return t
 
 
+def _host_resident(mf) -> bool:
+    return getattr(mf, "memory", "device") == "pinned"
+
+
 def _stream(device: int):
     import torch
     return torch.cuda.current_stream(device)
@@ -725,6 +729,11 @@ class Exchange:
         self.transport = "p2p"
         if self.mode == "process":
             self.transport = _transport()
+            if _host_resident(src_mf) or _host_resident(dst_mf):
+                # fabs in pinned host memory cannot be CUDA-IPC mapped by the
+                # peers: pack kernel (reads the host fabs over PCIe) -> device
+                # buffers -> message -> unpack kernel (writes the host fabs)
+                self.transport = "nccl"
             self.sync = _sync_mode(ctx) if self.transport == "p2p" else "stream"
         else:
             self.sync = "host" if self.mode == "thread" else "none"

@@ -31,7 +31,8 @@ def expected_wrapped(fab, ncomp, domain_row, periodic, seed, itemsize):
     import torch
     from paper_2403_12179_b200 import _native as N
     n = fab.raw().numel()
-    out = torch.empty(n, dtype=torch.int64 if itemsize == 8 else torch.int32, device=fab.data.device)
+    dev = fab.data.device if fab.data.is_cuda else torch.device("cuda", torch.cuda.current_device())  # host fabs
+    out = torch.empty(n, dtype=torch.int64 if itemsize == 8 else torch.int32, device=dev)
     fb = np.ascontiguousarray(np.asarray(fab.box.as_row(), np.int64))
     dom = np.ascontiguousarray(np.asarray(domain_row, np.int64))
     per = np.ascontiguousarray(np.asarray(list(periodic) + [0] * (3 - len(periodic)), np.int32))

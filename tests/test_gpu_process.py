@@ -46,7 +46,8 @@ def _worker(rank, world, port, q, n, b, nc, ng, env=None):
             from paper_2403_12179_b200.arena import Arena
             arena = Arena(0)
             arena.alloc(4096)
-        mf = amr.MultiFab(ba, dm, nc, ng, geom, arena=arena)
+        memory = "pinned" if os.environ.get("GHX_TEST_PINNED") else "device"  # host-resident fabs
+        mf = amr.MultiFab(ba, dm, nc, ng, geom, arena=arena, memory=memory)
         mf.fill_hash(inputs.SEED, dom)
         torch.cuda.synchronize()
         ctx = amr.current_ctx()
@@ -58,7 +59,7 @@ def _worker(rank, world, port, q, n, b, nc, ng, env=None):
         for gi in mf.local_indices:
             f = mf.fabs[gi]
             exp = expected_wrapped(f, nc, dom.as_row(), (1, 1, 1), inputs.SEED, 8)
-            bad += int((device_bits(f) != exp).sum().item())
+            bad += int((device_bits(f).to(exp.device) != exp).sum().item())
         stats = {f"{s}->{d}": (s1[(s, d)][0] - s0[(s, d)][0], s1[(s, d)][1] - s0[(s, d)][1])
                  for (s, d) in s1 if s1[(s, d)] != s0[(s, d)]}
         dist.barrier()
@@ -78,11 +79,15 @@ CASES = [("C1", 64, 32, 1, 1, "C1_x2", {"GHX_REMOTE": "direct"}), ("C3", 512, 12
          ("C1", 64, 32, 1, 1, "C1_x2", {"GHX_TRANSPORT": "nccl"}),
          ("C3", 512, 128, 8, 2, "C3_x2", {"GHX_TRANSPORT": "nccl"}),
          # fab storage at an offset inside an arena slab: IPC maps whole allocations
-         ("C1", 64, 32, 1, 1, "C1_x2", {"GHX_TEST_ARENA": "1", "GHX_REMOTE": "direct"})]
+         ("C1", 64, 32, 1, 1, "C1_x2", {"GHX_TEST_ARENA": "1", "GHX_REMOTE": "direct"}),
+         # fabs in pinned host memory: pack -> message -> unpack, kernels over PCIe
+         ("C1", 64, 32, 1, 1, "C1_x2", {"GHX_TEST_PINNED": "1"}),
+         ("C3", 512, 128, 8, 2, "C3_x2", {"GHX_TEST_PINNED": "1"})]
 
 
 @pytest.mark.parametrize("cfg", CASES, ids=["C1-ipc-direct", "C3-ipc-packed", "C3-ipc-direct", "C1-devbarrier-packed",
-                                            "C1-fallback", "C3-fallback", "C1-arena-ipc"])
+                                            "C1-fallback", "C3-fallback", "C1-arena-ipc", "C1-pinned",
+                                            "C3-pinned"])
 def test_two_processes_one_gpu(cfg):
     _run(cfg, 2)
 

@@ -27,4 +27,5 @@ from . import amr  # noqa: E402,F401
 from .amr import LINEAR, PIECEWISE_CONSTANT, average_down, fill_patch, interp_box  # noqa: E402,F401
 from . import heat  # noqa: E402,F401
 from . import arena  # noqa: E402,F401
+from . import kernels  # noqa: E402,F401
 from .heat import advance_level, heat_step  # noqa: E402,F401

@@ -940,8 +940,16 @@ def _execute_plan(plan: CommPlan, src_mf: MultiFab, dst_mf: MultiFab, scomp: int
     torch stream of the MultiFab's device; returns when the data is in
     place (the reference API is synchronous).  ``backend`` is accepted for
     signature compatibility only: there is one execution path, the fused
-    CUDA kernel."""
-    exchange_for(plan, src_mf, dst_mf, scomp, dcomp, ncomp, ctx).run()
+    CUDA kernel; a reference-style backend object (kernels.Backend) gets
+    this call's device launches added to its ``launch_counter``."""
+    ex = exchange_for(plan, src_mf, dst_mf, scomp, dcomp, ncomp, ctx)
+    ex.run()
+    if backend is not None and hasattr(backend, "launch_counter"):
+        bump = getattr(backend, "_bump", None)
+        if bump is not None:
+            bump(ex.launches_per_call)
+        else:
+            backend.launch_counter += ex.launches_per_call
 
 
 def prepare_fill_boundary(mf: MultiFab, geom: Geometry | None = None) -> Exchange:

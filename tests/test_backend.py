@@ -1,0 +1,41 @@
+"""The reference's backend handle (kernels.Backend) on the exchange API:
+accepted for signature compatibility, "gpu" and other kinds raise like the
+reference (tests/test_kernels.py:202-205), and launch_counter counts the
+device launches of each call."""
+
+import pytest
+
+import paper_2403_12179_b200 as amr
+from paper_2403_12179_b200 import kernels
+
+
+def test_backend_kinds():
+    assert kernels.Backend().kind == kernels.SERIAL
+    assert kernels.Backend(kernels.CPU_PARALLEL, 3).nworkers == 3
+    with pytest.raises(ValueError):
+        kernels.Backend("gpu")
+    with pytest.raises(ValueError):
+        kernels.Backend(kernels.SERIAL, -1)
+    b = kernels.Backend()
+    kernels.set_default_backend(b)
+    assert kernels.default_backend() is b
+
+
+@pytest.mark.gpu
+def test_backend_launch_counter_single_rank():
+    amr.config.set_spacedim(3)
+    dom = amr.Box((0, 0, 0), (31, 31, 31))
+    geom = amr.Geometry(dom, (0.0,) * 3, (1.0,) * 3, (True,) * 3)
+    ba = amr.decompose(dom, 16)
+    dm = amr.DistributionMapping.round_robin(len(ba), 1)
+    mf = amr.MultiFab(ba, dm, 2, 1, geom)
+    mf.setval(1.0)
+    b = kernels.Backend(kernels.CPU_PARALLEL)
+    amr.fill_boundary(mf, geom, backend=b)
+    assert b.launch_counter == 1  # one fused launch; the reference's single local phase is one dispatch too
+    src = amr.MultiFab(ba, dm, 2, 0)
+    src.setval(2.0)
+    amr.parallel_copy(mf, src, backend=b)
+    assert b.launch_counter == 2
+    amr.fill_boundary(mf, geom)  # no backend: nothing counted
+    assert b.launch_counter == 2

@@ -216,7 +216,7 @@ def _average_down_direct(fine: MultiFab, coarse: MultiFab, tmp: MultiFab, ratio:
         N.check(N.lib.ghx_average_down_prepare(C.c_void_p(rows.ctypes.data), len(rows), fine.ncomp,
                                                N.i32p(_ratio3(ratio)), config.spacedim, fine.dtype.itemsize,
                                                fine.device, C.byref(h)))
-        xf = fine._peer_cache[key] = _Xfer(h.value, fine.device)
+        xf = comm.cache_put(fine, key, _Xfer(h.value, fine.device), coarse)
     xf.run()
 
 
@@ -391,8 +391,8 @@ def _region_gather(fine: MultiFab, coarse: MultiFab, coarse_geom: Geometry, key,
                     slots.append((gi, need))
         plan = comm.build_gather_plan(list(enumerate(b for _, b in slots)), [0] * len(slots), coarse, coarse_geom)
         dst = _RegionSet(owned, slots, coarse)
-        ex = fine._peer_cache[gkey] = (plan, dst, None if plan.is_empty else
-                                       comm.exchange_for(plan, coarse, dst, 0, 0, coarse.ncomp))
+        ex = comm.cache_put(fine, gkey, (plan, dst, None if plan.is_empty else
+                                         comm.exchange_for(plan, coarse, dst, 0, 0, coarse.ncomp)), coarse)
     return ex[2]
 
 

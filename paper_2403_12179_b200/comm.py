@@ -720,7 +720,10 @@ class Exchange:
                  ncomp: int, ctx):
         if src_mf.dtype != dst_mf.dtype:
             raise ValueError("source and destination MultiFabs must share the real type")
-        self.plan, self.src, self.dst, self.ctx = plan, src_mf, dst_mf, ctx
+        # a cached exchange lives on dst and must not keep a distinct source
+        # alive (exchange_for evicts it when the source is collected)
+        self._src = src_mf if src_mf is dst_mf else weakref.ref(src_mf)
+        self.plan, self.dst, self.ctx = plan, dst_mf, ctx
         self.scomp, self.dcomp, self.ncomp = scomp, dcomp, ncomp
         self.item = dst_mf.dtype.itemsize
         self.device = dst_mf.device
@@ -761,6 +764,13 @@ class Exchange:
         self.local_cells = int(row[me])
         self.remote_cells = int(sum(row[d] for d in range(plan.nranks) if d != me))
         self.ghost_bytes = int(plan.pair_cells.sum()) * ncomp * self.item  # whole job, counted once
+
+    @property
+    def src(self) -> MultiFab:
+        s = self._src if not isinstance(self._src, weakref.ref) else self._src()
+        if s is None:
+            raise RuntimeError("the source MultiFab of this exchange has been released")
+        return s
 
     # -- packed push (process mode) ---------------------------------------
     def _init_packed(self):
@@ -930,8 +940,27 @@ def exchange_for(plan: CommPlan, src_mf: MultiFab, dst_mf: MultiFab, scomp: int,
            _transport() if ctx.kind == "process" else None)
     ex = dst_mf._peer_cache.get(key)
     if ex is None:
-        ex = dst_mf._peer_cache[key] = Exchange(plan, src_mf, dst_mf, scomp, dcomp, ncomp, ctx)
+        ex = cache_put(dst_mf, key, Exchange(plan, src_mf, dst_mf, scomp, dcomp, ncomp, ctx), src_mf)
     return ex
+
+
+def cache_put(owner, key, value, *deps):
+    """``owner._peer_cache[key] = value``, dropped again when any of ``deps``
+    (other MultiFabs the entry was built for) is garbage-collected, so a
+    long-lived MultiFab does not accumulate executors, device tables or
+    staging slabs for partners that no longer exist."""
+    owner._peer_cache[key] = value
+    oref = weakref.ref(owner)
+    for d in deps:
+        if d is not None and d is not owner:
+            weakref.finalize(d, _cache_drop, oref, key)
+    return value
+
+
+def _cache_drop(oref, key) -> None:
+    o = oref()
+    if o is not None:
+        o._peer_cache.pop(key, None)
 
 
 def _execute_plan(plan: CommPlan, src_mf: MultiFab, dst_mf: MultiFab, scomp: int, dcomp: int,
@@ -1078,6 +1107,7 @@ def _gather_set(plan: CommPlan, dst_fabs: list, dst_ranks: list, src: MultiFab) 
     if fs is None:
         fs = plan._execs[key] = _FabSet([b for _, b in dst_fabs], list(dst_ranks), src.ncomp, src.dtype,
                                         src.device, ctx.rank, len(src.ngrow))
+        weakref.finalize(src, plan._execs.pop, key, None)  # the target slab goes with its source
     return fs
 
 

@@ -79,7 +79,7 @@ def _stencil(u: MultiFab, w: MultiFab, dt: float, diffusivity: float, geom: Geom
     key = ("advance", part, w.uid, tuple(coef.tolist()))
     xf = u._peer_cache.get(key)
     if xf is None:
-        xf = u._peer_cache[key] = _prepare(u, w, coef, part)
+        xf = comm.cache_put(u, key, _prepare(u, w, coef, part), w)
     return xf
 
 

@@ -39,3 +39,32 @@ def test_backend_launch_counter_single_rank():
     assert b.launch_counter == 2
     amr.fill_boundary(mf, geom)  # no backend: nothing counted
     assert b.launch_counter == 2
+
+
+@pytest.mark.gpu
+def test_cached_exchanges_do_not_keep_sources_alive():
+    """A long-lived destination copied from a fresh source each call (a
+    regrid loop) must not accumulate the sources' device memory: the
+    cached executors evict themselves when their source is collected."""
+    import gc
+    import weakref
+    import torch
+    amr.config.set_spacedim(3)
+    dom = amr.Box((0, 0, 0), (31, 31, 31))
+    geom = amr.Geometry(dom, (0.0,) * 3, (1.0,) * 3, (True,) * 3)
+    ba = amr.decompose(dom, 16)
+    dm = amr.DistributionMapping.round_robin(len(ba), 1)
+    dst = amr.MultiFab(ba, dm, 1, 1, geom)
+    refs = []
+    for it in range(4):
+        src = amr.MultiFab(amr.decompose(dom, 8), amr.DistributionMapping.round_robin(64, 1), 1, 0)
+        src.setval(float(it))
+        amr.parallel_copy(dst, src)
+        assert float(dst.fabs[0].data[2, 2, 2, 0]) == float(it)
+        refs.append(weakref.ref(src))
+        del src
+        gc.collect()
+    torch.cuda.synchronize()
+    assert all(r() is None for r in refs)
+    assert sum(1 for k in dst._peer_cache if isinstance(k, tuple) and k[0] == "xchg") == 0
+    amr.fill_boundary(dst, geom)  # still works after the evictions

@@ -152,6 +152,8 @@ def average_down(fine: MultiFab, coarse: MultiFab, ratio: int, backend=None, *, 
     ratio = int(ratio)
     if ratio < 1:
         raise ValueError("ratio must be >= 1")
+    fine.check_open()
+    coarse.check_open()
     for b in fine.ba:
         if any(e % ratio for e in b.extents) or any(lo % ratio for lo in b.lo):
             raise ValueError(f"fine box {b} is not aligned to ratio {ratio}")
@@ -287,6 +289,8 @@ def fill_patch(fine: MultiFab, coarse: MultiFab, fine_geom: Geometry, coarse_geo
     slab) -> one interp launch over every (fab, region) job.  With a single
     rank the three steps are enqueued back to back on the current stream and
     the host waits once at the end."""
+    fine.check_open()
+    coarse.check_open()
     serial = comm.current_ctx().nranks == 1
     reach = 1 if scheme == LINEAR else 0
     key = comm.PlanKey(coarse.ba.uid, coarse.dm.uid, fine.ba.uid, fine.dm.uid, (reach,) * len(fine.ngrow),

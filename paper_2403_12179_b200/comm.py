@@ -935,6 +935,9 @@ def check_barriers() -> None:
 
 def exchange_for(plan: CommPlan, src_mf: MultiFab, dst_mf: MultiFab, scomp: int, dcomp: int, ncomp: int,
                  ctx=None) -> Exchange:
+    for m in (src_mf, dst_mf):
+        if hasattr(m, "check_open"):
+            m.check_open()
     ctx = ctx or current_ctx()
     key = ("xchg", plan.uid, src_mf.uid, scomp, dcomp, ncomp, ctx.kind, ctx.nranks,
            _transport() if ctx.kind == "process" else None)

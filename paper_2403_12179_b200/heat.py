@@ -71,6 +71,8 @@ def _prepare(u: MultiFab, w: MultiFab, coef: np.ndarray, part: str) -> _Xfer:
 
 
 def _stencil(u: MultiFab, w: MultiFab, dt: float, diffusivity: float, geom: Geometry, part: str) -> _Xfer:
+    u.check_open()
+    w.check_open()
     if u.ba is not w.ba and list(u.ba) != list(w.ba):
         raise ValueError("advance_level: u and unew must share the BoxArray")
     if min(u.ngrow) < 1 and part != "interior":

@@ -459,6 +459,15 @@ class MultiFab:
         self.fabs = {}
         self._slab = None
         self._ptrs = np.zeros(0, np.uint64)
+        self._peer_cache = {}  # cached executors hold device pointers into the released storage
+        self._closed = True
+
+    def check_open(self) -> None:
+        """Raise ValueError if close() released this MultiFab's storage (the
+        reference fails on its emptied ``fabs``; here cached device tables
+        would otherwise point at freed memory)."""
+        if getattr(self, "_closed", False):
+            raise ValueError("MultiFab has been closed")
 
     # -- exchange entry points named by the north star
     def fill_boundary(self, geom: Geometry | None = None, backend=None) -> None:

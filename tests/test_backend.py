@@ -68,3 +68,22 @@ def test_cached_exchanges_do_not_keep_sources_alive():
     assert all(r() is None for r in refs)
     assert sum(1 for k in dst._peer_cache if isinstance(k, tuple) and k[0] == "xchg") == 0
     amr.fill_boundary(dst, geom)  # still works after the evictions
+
+
+@pytest.mark.gpu
+def test_closed_multifab_raises_instead_of_touching_freed_memory():
+    amr.config.set_spacedim(3)
+    dom = amr.Box((0, 0, 0), (15, 15, 15))
+    geom = amr.Geometry(dom, (0.0,) * 3, (1.0,) * 3, (True,) * 3)
+    ba = amr.decompose(dom, 8)
+    dm = amr.DistributionMapping.round_robin(len(ba), 1)
+    mf = amr.MultiFab(ba, dm, 1, 1, geom)
+    other = amr.MultiFab(ba, dm, 1, 1, geom)
+    amr.fill_boundary(mf, geom)  # plan + executor cached
+    amr.parallel_copy(other, mf)
+    mf.close()
+    with pytest.raises(ValueError):
+        amr.fill_boundary(mf, geom)
+    with pytest.raises(ValueError):
+        amr.parallel_copy(other, mf)
+    amr.fill_boundary(other, geom)  # unaffected

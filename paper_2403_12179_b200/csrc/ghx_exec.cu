@@ -152,8 +152,15 @@ __device__ __forceinline__ u8x32 ld32(const void *p) {
          "=r"(r.w[3]), "=r"(r.w[4]), "=r"(r.w[5]), "=r"(r.w[6]), "=r"(r.w[7]) : "l"(p))
   return r;
 }
+// store cache qualifier (experiment knob, e.g. -DGHX_ST_Q='".cs"'); default: plain st.global
+#ifdef GHX_ST_Q
+#define GHX_ST_ASM 1
+#else
+#define GHX_ST_Q ""
+#define GHX_ST_ASM 0
+#endif
 __device__ __forceinline__ void st32(void *p, const uint32_t (&w)[8]) {
-  asm volatile("st.global.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(w[0]), "r"(w[1]), "r"(w[2]),
+  asm volatile("st.global" GHX_ST_Q ".v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(w[0]), "r"(w[1]), "r"(w[2]),
                "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
                : "memory");
 }
@@ -198,12 +205,22 @@ __device__ __forceinline__ void store_chunk(const DevTag &t, uint32_t start, int
     const uint32_t v = start + (uint32_t)(u * 32 + lane);
     if (v < t.nvec) {
       char *p = base + (vec_offset<false>(t, v) << vl);
+#if GHX_ST_ASM
+      if (vl == 4)
+        asm volatile("st.global" GHX_ST_Q ".v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(val[u].x), "r"(val[u].y),
+                     "r"(val[u].z), "r"(val[u].w) : "memory");
+      else if (vl == 3)
+        asm volatile("st.global" GHX_ST_Q ".v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(val[u].x), "r"(val[u].y) : "memory");
+      else
+        asm volatile("st.global" GHX_ST_Q ".u32 [%0], %1;" ::"l"(p), "r"(val[u].x) : "memory");
+#else
       if (vl == 4)
         *reinterpret_cast<uint4 *>(p) = val[u];
       else if (vl == 3)
         *reinterpret_cast<uint2 *>(p) = make_uint2(val[u].x, val[u].y);
       else
         *reinterpret_cast<uint32_t *>(p) = val[u].x;
+#endif
     }
   }
 }

@@ -47,6 +47,9 @@ CONFIGS = {
                desc="C3: 512^3 periodic domain, 128^3 boxes, ncomp 8, nghost 2, float64 FillBoundary"),
     "C4": dict(kind="fb", n=256, box=16, ncomp=4, ngrow=2,
                desc="C4: 256^3 periodic domain, 16^3 boxes (many-small-box stress), ncomp 4, nghost 2, float64 FillBoundary"),
+    # not a BASELINE config: the heat demo's exchange (the FillBoundary inside bench_amr.py --op heat)
+    "H1": dict(kind="fb", n=256, box=64, ncomp=1, ngrow=1,
+               desc="H1: 256^3 periodic domain, 64^3 boxes, ncomp 1, nghost 1, float64 FillBoundary (heat demo layout)"),
     "C5": dict(kind="pc", n=1024, src_box=64, box=128, ncomp=4, ngrow=0,
                desc="C5: ParallelCopy regrid 1024^3, 64^3-box layout -> 128^3-box layout, ncomp 4, float64"),
 }

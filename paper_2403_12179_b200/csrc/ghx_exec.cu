@@ -495,14 +495,16 @@ __global__ void __launch_bounds__(kThreads, GHX_MINB) ghx_copy_kernel(const DevT
     }
   }
   __syncwarp();
-  unsigned long long nb = 0;
-  if (lane == 0) nb = atomicAdd(counter, (unsigned long long)batch);
-  nb = __shfl_sync(0xffffffffu, nb, 0);
+  // first batch static (warp id), later ones dynamic from an offset of one
+  // batch per warp: no atomic -- and no contention of every warp on one
+  // counter -- on the critical path of a warp's first task
+  const unsigned long long static_tasks = (unsigned long long)gridDim.x * kWarps * batch;
+  unsigned long long nb = ((unsigned long long)blockIdx.x * kWarps + wib) * batch;
 #pragma unroll 1
   while (true) {
     const long long first = (long long)nb;
     if (first >= ntasks) break;
-    if (lane == 0) nb = atomicAdd(counter, (unsigned long long)batch);  // prefetch the next batch
+    if (lane == 0) nb = atomicAdd(counter, (unsigned long long)batch) + static_tasks;  // prefetch the next batch
     const int last = (int)min((long long)ntasks, first + batch);
     int4 tk = __ldg(tasks + first);
 #pragma unroll 1

@@ -1,5 +1,5 @@
 """Process-per-GPU host logic over torch.distributed with the gloo backend,
-world_size 2, on CPU: collectives of ProcessContext, identical plans on
+world_size 2 and 4, on CPU: collectives of ProcessContext, identical plans on
 every rank, reference message accounting, and the NCCL-fallback buffer
 contract (what rank s packs for rank d is exactly what d unpacks from s)."""
 
@@ -32,11 +32,11 @@ def _worker(rank, world, port, q):
         from paper_2403_12179_b200 import comm
         ctx = comm.current_ctx()
         assert ctx.kind == "process" and ctx.rank == rank and ctx.nranks == world
-        assert ctx.allgather(rank * 10) == [0, 10]
-        assert ctx.allreduce([amr.SUM, amr.MAX], [rank + 1, rank]) == (3.0, 1.0)
+        assert ctx.allgather(rank * 10) == [10 * r for r in range(world)]
+        assert ctx.allreduce([amr.SUM, amr.MAX], [rank + 1, rank]) == (world * (world + 1) / 2, world - 1.0)
         ctx.barrier()
         out = {}
-        # C3 at 2 ranks: plan + accounting vs the reference-generated fixture
+        # C3 at `world` ranks: plan + accounting vs the reference-generated fixture
         amr.config.set_spacedim(3)
         n, b, nc, ng = 512, 128, 8, 2
         dom = amr.Box((0, 0, 0), (n - 1,) * 3)
@@ -77,8 +77,8 @@ def _worker(rank, world, port, q):
         q.put((rank, "ERROR " + traceback.format_exc()))
 
 
-def test_process_group_world2_plans_accounting_and_buffers():
-    world = 2
+@pytest.mark.parametrize("world", [2, 4])
+def test_process_group_plans_accounting_and_buffers(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -90,7 +90,7 @@ def test_process_group_world2_plans_accounting_and_buffers():
         p.join(timeout=60)
     for r in range(world):
         assert not isinstance(res[r], str), res[r]
-    c = gu.case("C3_x2")
+    c = gu.case(f"C3_x{world}")
     got_pairs = {}
     for r in range(world):
         assert res[r]["segments"] == c["num_segments"]
@@ -100,4 +100,4 @@ def test_process_group_world2_plans_accounting_and_buffers():
         # host sync when both ranks share one device (this container: device 0)
         assert res[r]["sync"] == "host"
     assert got_pairs == c["pair_bytes"]
-    assert res[0]["digest"] == res[1]["digest"]
+    assert all(res[r]["digest"] == res[0]["digest"] for r in range(world))

@@ -1,5 +1,5 @@
 """Process-per-GPU host logic over torch.distributed with the gloo backend,
-world_size 2 and 4, on CPU: collectives of ProcessContext, identical plans on
+world_size 2, 4 and 8, on CPU: collectives of ProcessContext, identical plans on
 every rank, reference message accounting, and the NCCL-fallback buffer
 contract (what rank s packs for rank d is exactly what d unpacks from s)."""
 
@@ -77,7 +77,7 @@ def _worker(rank, world, port, q):
         q.put((rank, "ERROR " + traceback.format_exc()))
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_process_group_plans_accounting_and_buffers(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()

@@ -65,7 +65,7 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kSwapSlots = 8;
 #ifndef GHX_CHAIN_ROWS
-#define GHX_CHAIN_ROWS 64
+#define GHX_CHAIN_ROWS 16
 #endif
 constexpr int kChainRows = GHX_CHAIN_ROWS;  // rows per chain task
 #ifndef GHX_CHAIN_R

@@ -232,13 +232,16 @@ __device__ __forceinline__ void store_chunk(const DevTag &t, uint32_t start, int
 // half of SL from the high half of SA.  Both sectors end up holding
 // (SL.lo, SA.hi): each lane reads two whole sectors and writes them back
 // whole, so L2 never refills a partially written sector from HBM.
+#ifndef GHX_SWAP_PASSES
+#define GHX_SWAP_PASSES 2  // load/store passes per chunk (1: all kU vectors' loads before any store)
+#endif
 template <int LD>
 __device__ __forceinline__ void swap_chunk(const DevTag &t, uint32_t start, int lane) {
-  constexpr int kS = kU / 2;
+  constexpr int kS = kU / GHX_SWAP_PASSES;
   char *const da = reinterpret_cast<char *>(t.dst);
   char *const sl = reinterpret_cast<char *>(t.src);
 #pragma unroll 1
-  for (int h = 0; h < 2; ++h) {
+  for (int h = 0; h < GHX_SWAP_PASSES; ++h) {
     uint4 lo[kS], hi[kS];
 #pragma unroll
     for (int u = 0; u < kS; ++u) {

@@ -404,7 +404,10 @@ __device__ __forceinline__ void ring_task(const DevTag *__restrict__ tags, const
 // per row (cp.async.bulk with an mbarrier per warp), so a warp keeps
 // kBulkBytes in flight without holding them in registers.  Only for tags
 // whose source and destination do not alias (FillBoundary).
-constexpr int kBulkBytes = 8192;  // per-warp staging buffer (dynamic shared memory)
+#ifndef GHX_BULK_BYTES
+#define GHX_BULK_BYTES 8192
+#endif
+constexpr int kBulkBytes = GHX_BULK_BYTES;  // per-warp staging buffer (dynamic shared memory)
 
 __device__ __forceinline__ void bulk_task(const DevTag &t, uint32_t r0, uint32_t nrows, int lane, char *sbuf,
                                           uint64_t *bar, uint32_t &phase) {

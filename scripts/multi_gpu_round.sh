@@ -1,0 +1,27 @@
+#!/usr/bin/env bash
+# Multi-GPU measurement pass for a box with N >= 2 B200s (one process per
+# GPU, NCCL plumbing): weak-scaled C2, the north-star C3 and the C5 regrid at 2/4/8 GPUs
+# over the CUDA-IPC push (packed and direct remote rows, device barriers) and
+# the NCCL pack/send/unpack fallback, plus an ncu-free NVLink sanity probe.
+# Output: gpurun_out/multi/<config>_<transport>_<N>.json (one bench line each).
+#   bash scripts/multi_gpu_round.sh [max_gpus]
+set -u
+mkdir -p gpurun_out/multi
+export PYTHONDONTWRITEBYTECODE=1
+MAXG=${1:-$(nvidia-smi -L | wc -l)}
+nvidia-smi topo -m > gpurun_out/multi/topo.txt 2>&1
+port=29600
+for cfg in C2 C3 C5; do
+  steps=100; [ "$cfg" = C5 ] && steps=20
+  for n in 2 4 8; do
+    [ "$n" -le "$MAXG" ] || continue
+    for variant in "p2p:GHX_REMOTE=packed" "p2p:GHX_REMOTE=direct" "nccl:GHX_TRANSPORT=nccl"; do
+      tag=${variant%%:*}; envs=${variant#*:}
+      port=$((port + 1))
+      env $envs GHX_BARRIER_TIMEOUT_S=30 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n \
+        --master-addr 127.0.0.1 --master-port $port bench.py --gpus $n --config $cfg --steps $steps --warmup 5 --no-cpu --e2e-steps 2 \
+        > gpurun_out/multi/${cfg}_${tag}_${envs#*=}_$n.json 2> gpurun_out/multi/${cfg}_${tag}_${envs#*=}_$n.log
+      echo "$cfg n=$n $envs rc=$? $(python -c "import json,sys; d=json.load(open('gpurun_out/multi/${cfg}_${tag}_${envs#*=}_$n.json')); r=d['roofline'] or {}; print(d['value'], d['ms_per_step'], d['verified'], r.get('frac'), (r.get('nvlink') or {}).get('frac'), d['e2e']['value'])" 2>&1 | tail -1)"
+    done
+  done
+done

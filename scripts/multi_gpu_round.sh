@@ -2,7 +2,7 @@
 # Multi-GPU measurement pass for a box with N >= 2 B200s (one process per
 # GPU, NCCL plumbing): weak-scaled C2, the north-star C3 and the C5 regrid at 2/4/8 GPUs
 # over the CUDA-IPC push (packed and direct remote rows, device barriers) and
-# the NCCL pack/send/unpack fallback, plus an ncu-free NVLink sanity probe.
+# the NCCL pack/send/unpack fallback.
 # Output: gpurun_out/multi/<config>_<transport>_<N>.json (one bench line each).
 #   bash scripts/multi_gpu_round.sh [max_gpus]
 set -u

@@ -1062,8 +1062,7 @@ class _FabSet:
             total += -(-boxes[p].num_pts * self.ncomp * item // _ALIGN) * _ALIGN
         self._slab = Slab(max(total, 256), self.device) if self.local_indices else None
         if self._slab is not None and config.debug:  # fresh fabs are poisoned, like Fab()
-            N.check(N.lib.ghx_memset_u64(C.c_void_p(self._slab.ptr), config.POISON_BITS64 if item == 8
-                                         else (config.POISON_BITS32 << 32) | config.POISON_BITS32,
+            N.check(N.lib.ghx_memset_u64(C.c_void_p(self._slab.ptr), config.poison_word64(item),
                                          -(-total // 8), None))
         self.fabs = {p: Fab(boxes[p], self.ncomp, _slab=self._slab, _offset=offs[p]) for p in self.local_indices}
         self._ptrs = np.array([self.fabs[p].ptr for p in self.local_indices], np.uint64)

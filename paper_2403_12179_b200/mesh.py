@@ -151,8 +151,7 @@ class Fab:
             _slab = Slab(count * self.dtype.itemsize, dev, memory, arena=_native_arena(arena))
             _offset = 0
             if config.debug:
-                N.check(N.lib.ghx_memset_u64(C.c_void_p(_slab.ptr), config.POISON_BITS64 if self.dtype.itemsize == 8
-                                             else (config.POISON_BITS32 << 32) | config.POISON_BITS32,
+                N.check(N.lib.ghx_memset_u64(C.c_void_p(_slab.ptr), config.poison_word64(self.dtype.itemsize),
                                              -(-count * self.dtype.itemsize // 8), None))
         self._slab = _slab
         self.device = _slab.device
@@ -250,7 +249,12 @@ class FabView:
                 loc.append(z)
             else:
                 scalar = False
-                loc.append(_torch().as_tensor(np.asarray(g) - base, device=self._a.device))
+                z = np.asarray(g) - base
+                # debug builds check vector indices too (reference mesh.py:172-174);
+                # otherwise negative offsets wrap like numpy/torch fancy indexing
+                if config.debug and z.size and (int(z.min()) < 0 or int(z.max()) >= self._a.shape[axis]):
+                    raise IndexError(f"vector index outside the fab on axis {axis}")
+                loc.append(_torch().as_tensor(z, device=self._a.device))
         return tuple(loc) + (comp,), scalar
 
     def __getitem__(self, key):
@@ -415,8 +419,7 @@ class MultiFab:
             return
         self._slab = Slab(total, self.device, self.memory, arena=_native_arena(self.arena))
         if config.debug:
-            N.check(N.lib.ghx_memset_u64(C.c_void_p(self._slab.ptr), config.POISON_BITS64 if item == 8
-                                         else (config.POISON_BITS32 << 32) | config.POISON_BITS32,
+            N.check(N.lib.ghx_memset_u64(C.c_void_p(self._slab.ptr), config.poison_word64(item),
                                          total // 8, None))
         for i in self.local_indices:
             self.fabs[i] = Fab(grow(self.ba[i], self.ngrow), self.ncomp, _slab=self._slab, _offset=offs[i])

@@ -54,6 +54,13 @@ extern "C" {
  * receive buffer); the receiver then runs GHX_EXEC_UNPACK_PACKED. */
 #define GHX_EXEC_PUSH_PACKED 4
 #define GHX_EXEC_UNPACK_PACKED 5
+/* the same pair with EVERY remote tag packed (no peer fab pointers needed):
+ * used when fabs live in pinned host memory, which peers cannot IPC-map --
+ * the sender's kernel reads its host fabs and stores the packed rows into
+ * the peer's IPC-mapped DEVICE receive buffer; the receiver unpacks into
+ * its own host fabs. */
+#define GHX_EXEC_PUSH_PACKED_ALL 6
+#define GHX_EXEC_UNPACK_PACKED_ALL 7
 
 typedef struct ghx_plan ghx_plan;
 typedef struct ghx_exec ghx_exec;

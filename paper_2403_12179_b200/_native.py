@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("GHX_LIB") or os.path.join(_HERE, "_lib", "libghostx.s
 GHX_OK, GHX_EINVAL, GHX_ECUDA, GHX_ENOMEM, GHX_EOVERLAP = 0, 1, 2, 3, 4
 MODE_FILL_BOUNDARY, MODE_PARALLEL_COPY = 0, 1
 EXEC_DIRECT, EXEC_LOCAL, EXEC_PACK, EXEC_UNPACK, EXEC_PUSH_PACKED, EXEC_UNPACK_PACKED = 0, 1, 2, 3, 4, 5
+EXEC_PUSH_PACKED_ALL, EXEC_UNPACK_PACKED_ALL = 6, 7
 
 P = C.c_void_p
 I32 = C.c_int32

@@ -730,13 +730,9 @@ class Exchange:
         me = ctx.rank
         self.mode = "serial" if ctx.nranks == 1 else ctx.kind
         self.transport = "p2p"
+        host = _host_resident(src_mf) or _host_resident(dst_mf)
         if self.mode == "process":
             self.transport = _transport()
-            if _host_resident(src_mf) or _host_resident(dst_mf):
-                # fabs in pinned host memory cannot be CUDA-IPC mapped by the
-                # peers: pack kernel (reads the host fabs over PCIe) -> device
-                # buffers -> message -> unpack kernel (writes the host fabs)
-                self.transport = "nccl"
             self.sync = _sync_mode(ctx) if self.transport == "p2p" else "stream"
         else:
             self.sync = "host" if self.mode == "thread" else "none"
@@ -744,6 +740,13 @@ class Exchange:
         self.unp = None
         if self.transport == "nccl":
             self._init_nccl()
+        elif self.mode == "process" and host:
+            # fabs in pinned host memory cannot be CUDA-IPC mapped by the
+            # peers: every remote tag is packed by the sender's kernel (reading
+            # its host fabs over PCIe) straight into the peer's IPC-mapped
+            # DEVICE receive slab; the receiver unpacks into its host fabs
+            self.remote = "packed_all"
+            self._init_packed(all_remote=True)
         elif self.mode == "process" and os.environ.get("GHX_REMOTE", "packed") == "packed":
             self.remote = "packed"
             self._init_packed()
@@ -773,15 +776,18 @@ class Exchange:
         return s
 
     # -- packed push (process mode) ---------------------------------------
-    def _init_packed(self):
-        """Narrow-row remote tags are packed by the sending kernel straight
-        into the receiver's CUDA-IPC-mapped receive slab (contiguous NVLink
-        stores); the receiver unpacks locally after the exit barrier.  Wide
-        rows, and all local tags, are stored directly into the fabs."""
+    def _init_packed(self, all_remote=False):
+        """Narrow-row remote tags (every remote tag with ``all_remote``) are
+        packed by the sending kernel straight into the receiver's
+        CUDA-IPC-mapped receive slab (contiguous NVLink stores); the receiver
+        unpacks locally after the exit barrier.  Wide rows, and all local
+        tags, are stored directly into the fabs."""
         plan, src_mf, dst_mf, ctx, me = self.plan, self.src, self.dst, self.ctx, self.ctx.rank
         a = (self.scomp, self.dcomp, self.ncomp)
-        self.ex = plan.executor(me, N.EXEC_PUSH_PACKED, src_mf, dst_mf, *a)
-        self.unp = plan.executor(me, N.EXEC_UNPACK_PACKED, src_mf, dst_mf, *a)
+        kp, ku = ((N.EXEC_PUSH_PACKED_ALL, N.EXEC_UNPACK_PACKED_ALL) if all_remote
+                  else (N.EXEC_PUSH_PACKED, N.EXEC_UNPACK_PACKED))
+        self.ex = plan.executor(me, kp, src_mf, dst_mf, *a)
+        self.unp = plan.executor(me, ku, src_mf, dst_mf, *a)
         item, n = self.item, plan.nranks
         recv_el = self.unp.buffer_elems
         offs, total = [], 0
@@ -807,7 +813,8 @@ class Exchange:
             send[r] = p.value + roffs[me]
         recv = np.asarray([self._recv.ptr + o for o in offs], np.uint64)
         bufs = np.concatenate([send, recv])
-        parts = _ipc_peers(ctx, dst_mf)
+        # with every remote tag packed, only this rank's own fabs are addressed
+        parts = [(dst_mf.local_indices, dst_mf._ptrs)] if all_remote else _ipc_peers(ctx, dst_mf)
         self.table = _table(self.ex, src_mf, parts, bufs)
         self.t_unp = _table(self.unp, src_mf, [(dst_mf.local_indices, dst_mf._ptrs)], bufs)
         weakref.finalize(self, _close_ipc, list(self._opened))
@@ -873,7 +880,7 @@ class Exchange:
     # -- launching ---------------------------------------------------------
     @property
     def launches_per_call(self) -> int:
-        return 3 if self.transport == "nccl" else (2 if self.remote == "packed" else 1)
+        return 3 if self.transport == "nccl" else (2 if self.remote in ("packed", "packed_all") else 1)
 
     def enqueue(self, stream: int) -> None:
         if self.transport == "nccl":

@@ -755,7 +755,7 @@ int swap_low(const ghx_exec *ex, int ia, int ib) {
   // fab must alias, which ghx_exec_run verifies for swap executors
   auto fab = [&](int i, bool src) { return src ? std::get<0>(ex->hkeys[i]) : std::get<1>(ex->hkeys[i]); };
   auto fits = [&](const DevTag &t1, int i1, const DevTag &t2, int i2) {
-    return (ex->kind <= GHX_EXEC_LOCAL || ex->kind == GHX_EXEC_PUSH_PACKED) && t1.vlog == 4 && t2.vlog == 4 && t1.nxv == 1 && t2.nxv == 1 &&
+    return (ex->kind <= GHX_EXEC_LOCAL || ex->kind == GHX_EXEC_PUSH_PACKED || ex->kind == GHX_EXEC_PUSH_PACKED_ALL) && t1.vlog == 4 && t2.vlog == 4 && t1.nxv == 1 && t2.nxv == 1 &&
            t1.ny == t2.ny && t1.nz == t2.nz && t1.nvec == t2.nvec && fab(i1, false) == fab(i2, true) &&
            fab(i1, true) == fab(i2, false) &&
            t1.dst_sy == t2.src_sy && t1.dst_sz == t2.src_sz && t1.dst_sc == t2.src_sc &&
@@ -1014,7 +1014,7 @@ int ghx_exec_create(const ghx_plan *plan, int32_t rank, int32_t kind, const int6
                     int32_t scomp, int32_t dcomp, int32_t ncomp, int32_t elem_bytes, int32_t device,
                     ghx_exec **out) {
   if (!plan || !out || (plan->nsrc && !src_fab_boxes) || (plan->ndst && !dst_fab_boxes) ||
-      rank < 0 || rank >= plan->nranks || kind < GHX_EXEC_DIRECT || kind > GHX_EXEC_UNPACK_PACKED ||
+      rank < 0 || rank >= plan->nranks || kind < GHX_EXEC_DIRECT || kind > GHX_EXEC_UNPACK_PACKED_ALL ||
       (elem_bytes != 4 && elem_bytes != 8) || ncomp < 1 || scomp < 0 || dcomp < 0 ||
       scomp + ncomp > src_ncomp_total || dcomp + ncomp > dst_ncomp_total) {
     set_error("ghx_exec_create: bad arguments");
@@ -1056,8 +1056,9 @@ int ghx_exec_create(const ghx_plan *plan, int32_t rank, int32_t kind, const int6
     const char *v = std::getenv("GHX_PACK_ROW_BYTES");
     return v ? (int64_t)std::atoll(v) : (int64_t)128;
   }();
+  const bool pack_all = kind == GHX_EXEC_PUSH_PACKED_ALL || kind == GHX_EXEC_UNPACK_PACKED_ALL;
   auto packable = [&](const Piece &p) {
-    return p.srank != p.drank && (p.dbox.hi[0] - p.dbox.lo[0] + 1) * elem_bytes <= pack_row_bytes;
+    return p.srank != p.drank && (pack_all || (p.dbox.hi[0] - p.dbox.lo[0] + 1) * elem_bytes <= pack_row_bytes);
   };
   int64_t bad = -1;
   for (size_t i = 0; i < plan->wtags.size(); ++i) {
@@ -1068,8 +1069,10 @@ int ghx_exec_create(const ghx_plan *plan, int32_t rank, int32_t kind, const int6
       case GHX_EXEC_LOCAL: take = p.srank == rank && p.drank == rank; break;
       case GHX_EXEC_PACK: take = p.srank == rank && p.drank != rank; dst_is_fab = false; break;
       case GHX_EXEC_UNPACK: take = p.drank == rank && p.srank != rank; src_is_fab = false; break;
-      case GHX_EXEC_PUSH_PACKED: take = p.srank == rank; dst_is_fab = !packable(p); break;
-      case GHX_EXEC_UNPACK_PACKED: take = p.drank == rank && packable(p); src_is_fab = false; break;
+      case GHX_EXEC_PUSH_PACKED:
+      case GHX_EXEC_PUSH_PACKED_ALL: take = p.srank == rank; dst_is_fab = !packable(p); break;
+      case GHX_EXEC_UNPACK_PACKED:
+      case GHX_EXEC_UNPACK_PACKED_ALL: take = p.drank == rank && packable(p); src_is_fab = false; break;
     }
     if (!take) continue;
     const Layout S = layout(src_fab_boxes + 6 * p.src, src_ncomp_total);

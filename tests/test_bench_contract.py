@@ -34,14 +34,44 @@ def _torchrun(nproc, args, env=None, timeout=600):
 
 def test_reference_arm_under_torchrun_prints_one_line():
     rc, lines, err = _torchrun(2, ["--impl", "reference", "--gpus", "2", "--steps", "3", "--warmup", "3",
-                                   "--cpu-seconds", "1"])
+                                   "--config", "C1"])
     assert rc == 0, err[-2000:]
     assert len(lines) == 1, lines
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["steps"] == 3 and d["warmup"] == 3
     assert d["value"] > 0 and d["unit"] == "GB/s" and d["higher_is_better"] is True
-    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    # the reference itself (baseline/_ref), not the port, with 2 simulated ranks
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "reference" and cb["cores"] >= 1 and cb["ranks"] == 2, cb
     assert d["e2e"] == {"value": d["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+
+
+def test_reference_arm_default_is_c3():
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "3", "--warmup", "3"],
+                       cwd=REPO, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, lines
+    d = json.loads(lines[0])
+    assert d["config"]["workload"].startswith("C3:") and d["config"]["domain"] == [512, 512, 512]
+    assert d["config"]["ghost_bytes_per_step"] == 830734336
+    assert d["cpu_baseline"]["kind"] == "reference" and d["steps"] == 3
+
+
+@pytest.mark.gpu
+def test_our_arm_one_gpu_default_c3():
+    r = subprocess.run([sys.executable, "bench.py", "--steps", "5", "--warmup", "3", "--e2e-steps", "2",
+                        "--cpu-seconds", "2", "--no-port"], cwd=REPO, capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, lines
+    d = json.loads(lines[0])
+    assert d["config"]["workload"].startswith("C3:") and d["n_gpus"] == 1 and d["scaling"] == "strong"
+    assert d["verified"] is True and d["gpu_launches"] == 5
+    assert d["roofline"]["bound"] == "hbm" and 0 < d["roofline"]["frac"] < 1.2
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "reference" and cb["bit_exact_vs_ours_fab0"] is True, cb
+    assert d["e2e"]["verified"] is True and d["e2e"]["h2d_bytes_per_step"] > 0
 
 
 @pytest.mark.gpu
@@ -51,7 +81,11 @@ def test_our_arm_two_ranks_on_one_gpu():
     assert rc == 0, err[-2000:]
     assert len(lines) == 1, lines
     d = json.loads(lines[0])
-    assert d["n_gpus"] == 2 and d["steps"] == 5 and d["warmup"] == 3 and d["scaling"] == "weak"
+    assert d["n_gpus"] == 2 and d["steps"] == 5 and d["warmup"] == 3 and d["scaling"] == "strong"
+    assert d["config"]["workload"].startswith("C3:")
     assert d["verified"] is True and d["value"] > 0 and d["gpu_launches"] > 0
-    assert d["roofline"]["bound"] in ("hbm", "nvlink") and d["roofline"]["frac"] > 0
+    # C3 over 2 GPUs: 142.7 MB per GPU each way over NVLink bounds the step
+    nv = d["roofline"]
+    assert nv["bound"] == "nvlink" and nv["frac"] > 0 and nv["peak"] == 770.0
+    assert nv["bytes_per_gpu_max_send_recv"] == 142737408 and "hbm" in nv
     assert d["e2e"]["verified"] is True and d["e2e"]["h2d_bytes_per_step"] > 0

@@ -129,6 +129,19 @@ void ghx_exec_free(ghx_exec *ex);
  * Base pointers must be 16-byte aligned. */
 int ghx_exec_run(ghx_exec *ex, void *const *ptrs, int64_t nptrs, void *stream);
 
+/* Pinned bindings.  ghx_exec_bind resolves a pointer table into the
+ * executor's own descriptor copy once (stream-ordered; completed before it
+ * returns unless the stream is capturing) and returns a binding id that
+ * ghx_exec_run_bound launches with no host table work.  A pinned binding is
+ * never recycled by ghx_exec_run, so CUDA graphs that captured its launch
+ * stay valid; ghx_exec_unbind releases the pin.  Every binding has its own
+ * scheduler counter, so different bindings of one executor may run on
+ * different streams concurrently; ONE binding must not be enqueued on two
+ * streams at once. */
+int ghx_exec_bind(ghx_exec *ex, void *const *ptrs, int64_t nptrs, void *stream, int64_t *binding);
+int ghx_exec_run_bound(ghx_exec *ex, int64_t binding, void *stream);
+int ghx_exec_unbind(ghx_exec *ex, int64_t binding);
+
 /* Introspection: tags, warp tasks, elements moved per run, algorithmic
  * bytes (read + write) per run, per-peer buffer elements (out[nranks]). */
 int ghx_exec_info(const ghx_exec *ex, int64_t *ntags, int64_t *ntasks, int64_t *elems,

@@ -47,6 +47,9 @@ _SIGS = {
     "ghx_exec_create": (C.c_int, [P, I32, I32, PI64, I32, PI64, I32, I32, I32, I32, I32, I32, C.POINTER(P)]),
     "ghx_exec_free": (None, [P]),
     "ghx_exec_run": (C.c_int, [P, C.POINTER(P), I64, P]),
+    "ghx_exec_bind": (C.c_int, [P, C.POINTER(P), I64, P, PI64]),
+    "ghx_exec_run_bound": (C.c_int, [P, I64, P]),
+    "ghx_exec_unbind": (C.c_int, [P, I64]),
     "ghx_exec_info": (C.c_int, [P, PI64, PI64, PI64, PI64]),
     "ghx_exec_buffer_elems": (C.c_int, [P, PI64]),
     "ghx_exec_detail": (C.c_int, [P, PI64]),

@@ -417,7 +417,10 @@ def _fp_overlap() -> bool:
 
 def _interp_xfer(fine: MultiFab, coarse: MultiFab, key, targets, owned, ratio: int, scheme: str) -> _Xfer:
     """The prepared interp launch of a fill_patch plan (validated once)."""
-    xkey = ("fill_patch_interp", key, int(ratio), scheme, fine.ncomp)
+    # the gather targets (``owned``) belong to this coarse MultiFab: two
+    # coarse MultiFabs of one layout (time levels, a rebuilt coarse) get
+    # their own prepared launch, dropped when that coarse MultiFab goes
+    xkey = ("fill_patch_interp", key, coarse.uid, int(ratio), scheme, fine.ncomp)
     xf = fine._peer_cache.get(xkey)
     if xf is None:
         if coarse.ncomp != fine.ncomp:
@@ -433,6 +436,6 @@ def _interp_xfer(fine: MultiFab, coarse: MultiFab, key, targets, owned, ratio: i
                 raise ValueError(f"insufficient coarse data: need {need} inside {cf.box}")
         if scheme not in (PIECEWISE_CONSTANT, LINEAR):
             raise ValueError(f"unknown interpolation scheme {scheme!r}")
-        xf = fine._peer_cache[xkey] = _prepare_interp(jobs, fine.ncomp, int(ratio), scheme, fine.dtype.itemsize,
-                                                      fine.device)
+        xf = comm.cache_put(fine, xkey, _prepare_interp(jobs, fine.ncomp, int(ratio), scheme, fine.dtype.itemsize,
+                                                        fine.device), coarse)
     return xf

@@ -459,6 +459,7 @@ class Executor:
             # requests); 8 CTAs measured best (C2 e2e 9.6 -> 7.4 ms)
             N.check(N.lib.ghx_exec_set_grid(h, int(os.environ.get("GHX_HOST_BLOCKS", "8")), 256))
         self.plan = plan
+        self.device = device
         self.nsrc = len(src_rows)
         self.ndst = len(dst_rows)
         self.nranks = plan.nranks
@@ -479,9 +480,22 @@ class Executor:
                                (int(v) for v in kinds)))
 
     def run(self, table: np.ndarray, stream: int) -> None:
+        """One launch with a raw pointer table (bound on the fly; an
+        unpinned binding may be recycled later)."""
         assert table.dtype == np.uint64 and table.size == self.nptrs
         N.check(N.lib.ghx_exec_run(self._h, table.ctypes.data_as(C.POINTER(C.c_void_p)), self.nptrs,
                                    C.c_void_p(stream)))
+
+    def bind(self, table: np.ndarray, stream: int | None = None) -> "Binding":
+        """Pin ``table`` (ghx_exec_bind): launches of the returned binding
+        skip all host table work and stay valid inside CUDA graphs."""
+        assert table.dtype == np.uint64 and table.size == self.nptrs
+        if stream is None:
+            stream = _stream(self.device).cuda_stream
+        bid = C.c_int64()
+        N.check(N.lib.ghx_exec_bind(self._h, table.ctypes.data_as(C.POINTER(C.c_void_p)), self.nptrs,
+                                    C.c_void_p(stream), C.byref(bid)))
+        return Binding(self, bid.value)
 
     def set_grid(self, blocks: int) -> None:
         N.check(N.lib.ghx_exec_set_grid(self._h, int(blocks), 256))
@@ -491,6 +505,27 @@ class Executor:
             if self._h:
                 N.lib.ghx_exec_free(self._h)
                 self._h = None
+        except Exception:
+            pass
+
+
+class Binding:
+    """A pinned pointer table of an Executor (released with the object)."""
+
+    __slots__ = ("ex", "id", "_h", "__weakref__")
+
+    def __init__(self, ex: Executor, bid: int):
+        self.ex, self.id = ex, bid
+        self._h = ex._h
+
+    def run(self, stream: int) -> None:
+        N.check(N.lib.ghx_exec_run_bound(self._h, self.id, C.c_void_p(stream)))
+
+    def __del__(self):
+        try:
+            if self.id:
+                N.lib.ghx_exec_unbind(self._h, self.id)
+                self.id = 0
         except Exception:
             pass
 
@@ -760,6 +795,8 @@ class Exchange:
                     self.psync = _process_sync(ctx)
             else:
                 self.table = None  # thread ranks: gathered per call
+        self._thread_bindings: dict = {}
+        self._pin()
         row = plan.pair_cells[me]
         self.messages = [(me, d, int(row[d]) * ncomp * self.item) for d in range(plan.nranks)
                          if d != me and row[d] > 0]
@@ -767,6 +804,29 @@ class Exchange:
         self.local_cells = int(row[me])
         self.remote_cells = int(sum(row[d] for d in range(plan.nranks) if d != me))
         self.ghost_bytes = int(plan.pair_cells.sum()) * ncomp * self.item  # whole job, counted once
+
+    def _bind_thread(self, gen, infos, stream: int) -> "Binding":
+        for (_, d, _, _) in infos:
+            if d != self.device and (self.device, d) not in _peer_enabled:
+                N.check(N.lib.ghx_enable_peer_access(self.device, d))
+                _peer_enabled.add((self.device, d))
+        table = _table(self.ex, self.src, [(idx, ptrs) for (_, _, idx, ptrs) in infos])
+        if len(self._thread_bindings) >= 4:  # bounded: drop the oldest generation
+            self._thread_bindings.pop(next(iter(self._thread_bindings)))
+        b = self._thread_bindings[gen] = self.ex.bind(table, stream)
+        return b
+
+    def _pin(self) -> None:
+        """Pin every pointer table this exchange launches with (once)."""
+        if self.transport == "nccl":
+            self.b_pack = self.pack.bind(self.t_pack)
+            self.b_local = self.local.bind(self.t_local)
+            self.b_unpack = self.unpack.bind(self.t_unpack)
+            return
+        if self.table is not None:
+            self.b_ex = self.ex.bind(self.table)
+        if self.unp is not None:
+            self.b_unp = self.unp.bind(self.t_unp)
 
     @property
     def src(self) -> MultiFab:
@@ -852,9 +912,18 @@ class Exchange:
         self.t_local = _table(self.local, src_mf, own, bufs)
 
     def _enqueue_nccl(self, stream: int) -> None:
+        # torch.distributed orders NCCL work (and gloo's host staging) against
+        # torch's CURRENT stream: make ``stream`` current for the whole
+        # sequence so the sends follow the pack and the unpack follows the
+        # receives on the caller's stream
+        import torch
+        with torch.cuda.stream(torch.cuda.ExternalStream(stream, device=torch.device("cuda", self.device))):
+            self._enqueue_nccl_current(stream)
+
+    def _enqueue_nccl_current(self, stream: int) -> None:
         import torch
         import torch.distributed as dist
-        self.pack.run(self.t_pack, stream)
+        self.b_pack.run(stream)
         if dist.get_backend() != "nccl":
             # host-staged message passing (gloo): test path for ranks sharing a GPU
             torch.cuda.current_stream(self.device).synchronize()
@@ -866,16 +935,16 @@ class Exchange:
                 q.wait()
             for r, t in recv.items():
                 self.recv_t[r].copy_(t)
-            self.local.run(self.t_local, stream)
-            self.unpack.run(self.t_unpack, stream)
+            self.b_local.run(stream)
+            self.b_unpack.run(stream)
             return
         ops = [dist.P2POp(dist.isend, t, r) for r, t in sorted(self.send_t.items())]
         ops += [dist.P2POp(dist.irecv, t, r) for r, t in sorted(self.recv_t.items())]
         reqs = dist.batch_isend_irecv(ops) if ops else []
-        self.local.run(self.t_local, stream)
+        self.b_local.run(stream)
         for q in reqs:
             q.wait()  # NCCL: the current stream waits, the host does not
-        self.unpack.run(self.t_unpack, stream)
+        self.b_unpack.run(stream)
 
     # -- launching ---------------------------------------------------------
     @property
@@ -886,13 +955,13 @@ class Exchange:
         if self.transport == "nccl":
             self._enqueue_nccl(stream)
         elif self.mode == "serial":
-            self.ex.run(self.table, stream)
+            self.b_ex.run(stream)
         elif self.mode == "process" and self.sync == "device":
             self.psync.barrier(stream)  # peers finished earlier work on their fabs
-            self.ex.run(self.table, stream)
+            self.b_ex.run(stream)
             self.psync.barrier(stream)  # every push into my fabs has landed
             if self.unp is not None:
-                self.unp.run(self.t_unp, stream)
+                self.b_unp.run(stream)
         else:
             raise RuntimeError(f"{self.mode} ranks with host synchronisation cannot enqueue; use run()")
 
@@ -901,22 +970,24 @@ class Exchange:
         ctx = self.ctx
         if self.mode == "thread":
             stream.synchronize()  # my earlier work on my fabs is done
-            infos = ctx.allgather((ctx.rank, self.dst.device, self.dst.local_indices, self.dst._ptrs))
-            for (_, d, _, _) in infos:
-                if d != self.device and (self.device, d) not in _peer_enabled:
-                    N.check(N.lib.ghx_enable_peer_access(self.device, d))
-                    _peer_enabled.add((self.device, d))
-            table = _table(self.ex, self.src, [(idx, ptrs) for (_, _, idx, ptrs) in infos])
-            self.ex.run(table, stream.cuda_stream)
+            # the peers' destination MultiFabs of this call (one object per
+            # rank); their fab pointers are fixed for a MultiFab's life, so the
+            # bound pointer table is cached per tuple of MultiFab uids
+            infos = ctx.allgather((self.dst.uid, self.dst.device, self.dst.local_indices, self.dst._ptrs))
+            gen = tuple(i[0] for i in infos)
+            b = self._thread_bindings.get(gen)
+            if b is None:
+                b = self._bind_thread(gen, infos, stream.cuda_stream)
+            b.run(stream.cuda_stream)
             stream.synchronize()
         elif self.mode == "process" and self.sync == "host":
             stream.synchronize()
             ctx.barrier()
-            self.ex.run(self.table, stream.cuda_stream)
+            self.b_ex.run(stream.cuda_stream)
             stream.synchronize()
             ctx.barrier()
             if self.unp is not None:
-                self.unp.run(self.t_unp, stream.cuda_stream)
+                self.b_unp.run(stream.cuda_stream)
                 stream.synchronize()
         else:
             self.enqueue(stream.cuda_stream)
@@ -1109,6 +1180,12 @@ def build_gather_plan(dst_fabs: list, dst_ranks: list, src: MultiFab, geom: Geom
     return CommPlan(h.value, nranks, len(src.ngrow), src.ba.ixtype)
 
 
+def _drop_plan_entry(pref, key) -> None:
+    p = pref()
+    if p is not None:
+        p._execs.pop(key, None)
+
+
 def _gather_set(plan: CommPlan, dst_fabs: list, dst_ranks: list, src: MultiFab) -> _FabSet:
     ctx = current_ctx()
     key = ("gather_set", src.uid, ctx.rank, src.ncomp)
@@ -1116,7 +1193,10 @@ def _gather_set(plan: CommPlan, dst_fabs: list, dst_ranks: list, src: MultiFab) 
     if fs is None:
         fs = plan._execs[key] = _FabSet([b for _, b in dst_fabs], list(dst_ranks), src.ncomp, src.dtype,
                                         src.device, ctx.rank, len(src.ngrow))
-        weakref.finalize(src, plan._execs.pop, key, None)  # the target slab goes with its source
+        # the target slab goes with its source; the finalizer holds the plan
+        # only weakly, so a plan built per call (gather_fabs(plan=None)) and its
+        # slab are freed when the caller drops it
+        weakref.finalize(src, _drop_plan_entry, weakref.ref(plan), key)
     return fs
 
 

@@ -39,6 +39,7 @@
 #include <cstring>
 #include <functional>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <new>
 #include <string>
@@ -662,21 +663,26 @@ struct ghx_exec {
   std::vector<int4> htasks;
   std::vector<int> hchain;  // chain tables (tag indices of consecutive seams)
   int *dchain = nullptr;
-  unsigned long long *dcounter = nullptr;
   DevTag *dtags = nullptr;
   int4 *dtasks = nullptr;
   void **dptrs = nullptr;
-  // bound descriptor tables, one per pointer table in use (e.g. the u and
-  // unew MultiFabs of a time loop share this executor): switching tables
-  // costs nothing after the first bind, and CUDA-graph replays never
-  // re-upload (binding 0 is dtags / dptrs above)
+  // Bound descriptor tables, one per pointer table in use: each holds its
+  // own copy of the descriptors with absolute addresses and its own
+  // scheduler counter.  Pinned bindings (ghx_exec_bind, held by a prepared
+  // exchange and baked into CUDA graphs) are never rebound; unpinned ones
+  // (ghx_exec_run with a raw table) are recycled least-recently-used, at
+  // most kMaxLoose of them.
   struct Binding {
     std::vector<void *> ptrs;
-    DevTag *dtags;
-    void **dptrs;
-    uint64_t last_use;
+    DevTag *dtags = nullptr;
+    void **dptrs = nullptr;
+    unsigned long long *counter = nullptr;
+    uint64_t last_use = 0;
+    int pins = 0;
+    int64_t id = 0;
   };
-  std::vector<Binding> bindings;
+  std::vector<std::unique_ptr<Binding>> bindings;
+  int64_t next_binding = 1;
   uint64_t uses = 0;
   int64_t nptrs = 0;
   int blocks = 0, threads = kThreads;
@@ -1177,6 +1183,21 @@ int ghx_exec_create(const ghx_plan *plan, int32_t rank, int32_t kind, const int6
 
 }  // extern "C"
 
+static int bulk_smem_attr(int device) {
+  static std::mutex mu;
+  static std::vector<char> done;
+  std::lock_guard<std::mutex> lk(mu);
+  if (device >= 0 && (size_t)device < done.size() && done[device]) return GHX_OK;
+  cudaError_t e = cudaFuncSetAttribute(ghx_copy_kernel<2, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kWarps * kBulkBytes);
+  if (e != cudaSuccess) return cuda_fail(e, "ghx_exec_run: bulk-row shared memory attribute");
+  if (device >= 0) {
+    if ((size_t)device >= done.size()) done.resize(device + 1, 0);
+    done[device] = 1;
+  }
+  return GHX_OK;
+}
+
 static int exec_upload(ghx_exec *ex) {
   if (ex->uploaded) return GHX_OK;
   apply_l2_fetch_limit();
@@ -1185,8 +1206,6 @@ static int exec_upload(ghx_exec *ex) {
     e = cudaMalloc(&ex->dtags, ex->htags.size() * sizeof(DevTag));
     if (e == cudaSuccess)
       e = cudaMemcpy(ex->dtags, ex->htags.data(), ex->htags.size() * sizeof(DevTag), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMalloc(&ex->dcounter, 2 * sizeof(unsigned long long));
-    if (e == cudaSuccess) e = cudaMemset(ex->dcounter, 0, 2 * sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaMalloc(&ex->dchain, std::max<size_t>(1, ex->hchain.size()) * sizeof(int));
     if (e == cudaSuccess && !ex->hchain.empty())
       e = cudaMemcpy(ex->dchain, ex->hchain.data(), ex->hchain.size() * sizeof(int), cudaMemcpyHostToDevice);
@@ -1216,14 +1235,14 @@ extern "C" {
 void ghx_exec_free(ghx_exec *ex) {
   if (!ex) return;
   DeviceGuard g(ex->device);
-  for (size_t i = 1; i < ex->bindings.size(); ++i) {
-    cudaFree(ex->bindings[i].dtags);
-    cudaFree(ex->bindings[i].dptrs);
+  for (auto &b : ex->bindings) {
+    cudaFree(b->dtags);
+    cudaFree(b->dptrs);
+    cudaFree(b->counter);
   }
   if (ex->dtags) cudaFree(ex->dtags);
   if (ex->dtasks) cudaFree(ex->dtasks);
   if (ex->dchain) cudaFree(ex->dchain);
-  if (ex->dcounter) cudaFree(ex->dcounter);
   if (ex->dptrs) cudaFree(ex->dptrs);
   delete ex;
 }
@@ -1329,78 +1348,91 @@ int ghx_exec_buffer_elems(const ghx_exec *ex, int64_t *per_peer) {
   return GHX_OK;
 }
 
-int ghx_exec_run(ghx_exec *ex, void *const *ptrs, int64_t nptrs, void *stream) {
-  if (!ex || (nptrs && !ptrs) || nptrs != ex->nptrs) {
-    set_error("ghx_exec_run: pointer table must have nsrc + ndst + 2*nranks entries");
-    return GHX_EINVAL;
-  }
-  if (ex->htasks.empty()) return GHX_OK;
-  std::lock_guard<std::mutex> lk(ex->mu);
-  DeviceGuard g(ex->device);
-  if (int rc = exec_upload(ex)) return rc;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  ghx_exec::Binding *bd = nullptr;
+}  // extern "C"
+
+namespace {
+
+constexpr size_t kMaxLoose = 4;
+
+int check_table(ghx_exec *ex, void *const *ptrs, int64_t nptrs) {
+  const uintptr_t amask = ex->nswap ? 31 : 15;
+  for (int64_t i = 0; i < nptrs; ++i)
+    if (reinterpret_cast<uintptr_t>(ptrs[i]) & amask) {
+      set_error("ghx_exec_run: base pointer " + std::to_string(i) + " is not " + std::to_string(amask + 1) +
+                "-byte aligned");
+      return GHX_EINVAL;
+    }
+  // every slot referenced by this rank's tags must be set
+  for (const DevTag &t : ex->htags)
+    if (!ptrs[t.src_ptr] || !ptrs[t.dst_ptr]) {
+      set_error("ghx_exec_run: a pointer slot used by this rank's tags is NULL");
+      return GHX_EINVAL;
+    }
+  // sector swaps read and write both fabs of a pair through one slot each
+  if (ex->nswap)
+    for (int32_t f = 0; f < std::min(ex->nsrc, ex->ndst); ++f)
+      if (ex->swap_fab.size() > (size_t)f && ex->swap_fab[f] && ptrs[f] != ptrs[ex->nsrc + f]) {
+        set_error("ghx_exec_run: FillBoundary executor needs src slot == dst slot for every fab");
+        return GHX_EINVAL;
+      }
+  return GHX_OK;
+}
+
+// Find the binding of this pointer table, or create one (recycling the
+// least recently used unpinned binding when kMaxLoose are in use).  The
+// bind (table upload + ghx_bind_kernel) is stream-ordered on st.  Caller
+// holds ex->mu.
+int find_or_bind(ghx_exec *ex, void *const *ptrs, int64_t nptrs, cudaStream_t st, ghx_exec::Binding **out) {
   for (auto &b : ex->bindings)
-    if (b.ptrs.size() == (size_t)nptrs && std::memcmp(b.ptrs.data(), ptrs, nptrs * sizeof(void *)) == 0) bd = &b;
-  if (!bd) {
-    const uintptr_t amask = ex->nswap ? 31 : 15;
-    for (int64_t i = 0; i < nptrs; ++i)
-      if (reinterpret_cast<uintptr_t>(ptrs[i]) & amask) {
-        set_error("ghx_exec_run: base pointer " + std::to_string(i) + " is not " + std::to_string(amask + 1) +
-                  "-byte aligned");
-        return GHX_EINVAL;
-      }
-    // every slot referenced by this rank's tags must be set
-    for (const DevTag &t : ex->htags)
-      if (!ptrs[t.src_ptr] || !ptrs[t.dst_ptr]) {
-        set_error("ghx_exec_run: a pointer slot used by this rank's tags is NULL");
-        return GHX_EINVAL;
-      }
-    // sector swaps read and write both fabs of a pair through one slot each
-    if (ex->nswap)
-      for (int32_t f = 0; f < std::min(ex->nsrc, ex->ndst); ++f)
-        if (ex->swap_fab.size() > (size_t)f && ex->swap_fab[f] && ptrs[f] != ptrs[ex->nsrc + f]) {
-          set_error("ghx_exec_run: FillBoundary executor needs src slot == dst slot for every fab");
-          return GHX_EINVAL;
-        }
-    constexpr size_t kMaxBindings = 4;
-    cudaError_t e = cudaSuccess;
-    if (ex->bindings.empty()) {
-      ex->bindings.push_back({{}, ex->dtags, ex->dptrs, 0});
-    } else if (ex->bindings.size() < kMaxBindings) {
-      ghx_exec::Binding nb{{}, nullptr, nullptr, 0};
-      e = cudaMalloc(&nb.dtags, std::max<size_t>(1, ex->htags.size()) * sizeof(DevTag));
-      if (e == cudaSuccess) e = cudaMalloc(&nb.dptrs, std::max<int64_t>(ex->nptrs, 1) * sizeof(void *));
-      if (e == cudaSuccess && !ex->htags.empty())
-        e = cudaMemcpyAsync(nb.dtags, ex->dtags, ex->htags.size() * sizeof(DevTag), cudaMemcpyDeviceToDevice, st);
-      if (e != cudaSuccess) {
-        if (nb.dtags) cudaFree(nb.dtags);
-        if (nb.dptrs) cudaFree(nb.dptrs);
-        return cuda_fail(e, "ghx_exec_run: binding");
-      }
-      ex->bindings.push_back(nb);
-    } else {  // reuse the least recently used binding (stream-ordered rebind)
-      size_t lru = 0;
-      for (size_t i = 1; i < ex->bindings.size(); ++i)
-        if (ex->bindings[i].last_use < ex->bindings[lru].last_use) lru = i;
-      std::swap(ex->bindings[lru], ex->bindings.back());
+    if (b->ptrs.size() == (size_t)nptrs && std::memcmp(b->ptrs.data(), ptrs, nptrs * sizeof(void *)) == 0) {
+      *out = b.get();
+      return GHX_OK;
     }
-    bd = &ex->bindings.back();
-    bd->ptrs.assign(ptrs, ptrs + nptrs);
-    // pageable source: the copy has consumed the host table when this returns
-    e = cudaMemcpyAsync(bd->dptrs, bd->ptrs.data(), nptrs * sizeof(void *), cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess) {
-      const int n = (int)ex->htags.size();
-      ghx_bind_kernel<<<std::min(1184, (n + 255) / 256), 256, 0, st>>>(bd->dtags, n, bd->dptrs);
-      e = cudaGetLastError();
-    }
+  if (int rc = check_table(ex, ptrs, nptrs)) return rc;
+  ghx_exec::Binding *bd = nullptr;
+  size_t loose = 0;
+  for (auto &b : ex->bindings) loose += b->pins == 0;
+  if (loose >= kMaxLoose) {  // recycle the LRU unpinned binding (stream-ordered rebind)
+    for (auto &b : ex->bindings)
+      if (b->pins == 0 && (!bd || b->last_use < bd->last_use)) bd = b.get();
+  } else {
+    std::unique_ptr<ghx_exec::Binding> nb(new ghx_exec::Binding());
+    cudaError_t e = cudaMalloc(&nb->dtags, std::max<size_t>(1, ex->htags.size()) * sizeof(DevTag));
+    if (e == cudaSuccess) e = cudaMalloc(&nb->dptrs, std::max<int64_t>(ex->nptrs, 1) * sizeof(void *));
+    if (e == cudaSuccess) e = cudaMalloc(&nb->counter, 2 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemsetAsync(nb->counter, 0, 2 * sizeof(unsigned long long), st);
+    if (e == cudaSuccess && !ex->htags.empty())
+      e = cudaMemcpyAsync(nb->dtags, ex->dtags, ex->htags.size() * sizeof(DevTag), cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) {
-      bd->ptrs.clear();
-      return cuda_fail(e, "ghx_exec_run: pointer bind");
+      cudaFree(nb->dtags);
+      cudaFree(nb->dptrs);
+      cudaFree(nb->counter);
+      return cuda_fail(e, "ghx_exec_run: binding");
     }
+    nb->id = ex->next_binding++;
+    bd = nb.get();
+    ex->bindings.push_back(std::move(nb));
   }
+  bd->ptrs.assign(ptrs, ptrs + nptrs);
+  // pageable source: the copy has consumed the host table when this returns
+  cudaError_t e = cudaMemcpyAsync(bd->dptrs, bd->ptrs.data(), nptrs * sizeof(void *), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) {
+    const int n = (int)ex->htags.size();
+    if (n) ghx_bind_kernel<<<std::min(1184, (n + 255) / 256), 256, 0, st>>>(bd->dtags, n, bd->dptrs);
+    e = cudaGetLastError();
+  }
+  if (e != cudaSuccess) {
+    bd->ptrs.clear();
+    return cuda_fail(e, "ghx_exec_run: pointer bind");
+  }
+  *out = bd;
+  return GHX_OK;
+}
+
+int launch(ghx_exec *ex, ghx_exec::Binding *bd, cudaStream_t st) {
   bd->last_use = ++ex->uses;
   DevTag *const dtags = bd->dtags;
+  unsigned long long *const counter = bd->counter;
   const int ntasks = (int)ex->htasks.size();
   // tasks per atomic grab: single tasks balance the latency-bound seam work
   // best (FillBoundary plans, measured), long streaming task lists
@@ -1414,27 +1446,100 @@ int ghx_exec_run(ghx_exec *ex, void *const *ptrs, int64_t nptrs, void *stream) {
     return GHX_EINVAL;
   }
   if (ex->nbulk) {
-    static bool attr_set = false;
-    if (!attr_set) {
-      cudaFuncSetAttribute(ghx_copy_kernel<2, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           kWarps * kBulkBytes);
-      attr_set = true;
-    }
+    // the dynamic shared memory limit is a per-device (per-context) function
+    // attribute: set it once on every device that launches bulk rows
+    if (int rc = bulk_smem_attr(ex->device)) return rc;
     ghx_copy_kernel<2, false, true><<<ex->blocks, ex->threads, kWarps * kBulkBytes, st>>>(
-        dtags, ex->dtasks, ntasks, ex->dchain, ex->dcounter, batch);
+        dtags, ex->dtasks, ntasks, ex->dchain, counter, batch);
   } else if (ex->nring) {  // ring tasks present: the ring-capable instantiation
-    ghx_copy_kernel<2, true><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, ex->dcounter, batch);
+    ghx_copy_kernel<2, true><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, counter, batch);
   } else switch (ld) {
-    case 0: ghx_copy_kernel<0><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, ex->dcounter, batch); break;
-    case 1: ghx_copy_kernel<1><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, ex->dcounter, batch); break;
-    case 2: ghx_copy_kernel<2><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, ex->dcounter, batch); break;
-    case 3: ghx_copy_kernel<3><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, ex->dcounter, batch); break;
-    default: ghx_copy_kernel<4><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, ex->dcounter, batch); break;
+    case 0: ghx_copy_kernel<0><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, counter, batch); break;
+    case 1: ghx_copy_kernel<1><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, counter, batch); break;
+    case 2: ghx_copy_kernel<2><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, counter, batch); break;
+    case 3: ghx_copy_kernel<3><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, counter, batch); break;
+    default: ghx_copy_kernel<4><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, counter, batch); break;
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "ghx_exec_run: launch");
   g_launches.fetch_add(1);
   return GHX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ghx_exec_run(ghx_exec *ex, void *const *ptrs, int64_t nptrs, void *stream) {
+  if (!ex || (nptrs && !ptrs) || nptrs != ex->nptrs) {
+    set_error("ghx_exec_run: pointer table must have nsrc + ndst + 2*nranks entries");
+    return GHX_EINVAL;
+  }
+  if (ex->htasks.empty()) return GHX_OK;
+  std::lock_guard<std::mutex> lk(ex->mu);
+  DeviceGuard g(ex->device);
+  if (int rc = exec_upload(ex)) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  ghx_exec::Binding *bd = nullptr;
+  if (int rc = find_or_bind(ex, ptrs, nptrs, st, &bd)) return rc;
+  return launch(ex, bd, st);
+}
+
+int ghx_exec_bind(ghx_exec *ex, void *const *ptrs, int64_t nptrs, void *stream, int64_t *binding) {
+  if (!ex || !binding || (nptrs && !ptrs) || nptrs != ex->nptrs) {
+    set_error("ghx_exec_bind: pointer table must have nsrc + ndst + 2*nranks entries");
+    return GHX_EINVAL;
+  }
+  *binding = 0;
+  if (ex->htasks.empty()) return GHX_OK;  // nothing to run: binding 0 is a no-op
+  std::lock_guard<std::mutex> lk(ex->mu);
+  DeviceGuard g(ex->device);
+  if (int rc = exec_upload(ex)) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  ghx_exec::Binding *bd = nullptr;
+  if (int rc = find_or_bind(ex, ptrs, nptrs, st, &bd)) return rc;
+  bd->pins += 1;
+  *binding = bd->id;
+  // a pinned binding may be launched on any stream later: make the bind
+  // complete now unless this stream is being captured into a graph (then
+  // the bind is part of the graph, ahead of the launch)
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  if (cs == cudaStreamCaptureStatusNone) {
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "ghx_exec_bind: synchronize");
+  }
+  return GHX_OK;
+}
+
+int ghx_exec_run_bound(ghx_exec *ex, int64_t binding, void *stream) {
+  if (!ex) {
+    set_error("ghx_exec_run_bound: null handle");
+    return GHX_EINVAL;
+  }
+  if (ex->htasks.empty()) return GHX_OK;
+  std::lock_guard<std::mutex> lk(ex->mu);
+  DeviceGuard g(ex->device);
+  for (auto &b : ex->bindings)
+    if (b->id == binding && b->pins > 0) return launch(ex, b.get(), static_cast<cudaStream_t>(stream));
+  set_error("ghx_exec_run_bound: unknown or released binding " + std::to_string(binding));
+  return GHX_EINVAL;
+}
+
+int ghx_exec_unbind(ghx_exec *ex, int64_t binding) {
+  if (!ex) {
+    set_error("ghx_exec_unbind: null handle");
+    return GHX_EINVAL;
+  }
+  if (binding == 0) return GHX_OK;
+  std::lock_guard<std::mutex> lk(ex->mu);
+  for (auto &b : ex->bindings)
+    if (b->id == binding && b->pins > 0) {
+      b->pins -= 1;  // stays allocated; recyclable once unpinned
+      return GHX_OK;
+    }
+  set_error("ghx_exec_unbind: unknown or released binding " + std::to_string(binding));
+  return GHX_EINVAL;
 }
 
 }  // extern "C"

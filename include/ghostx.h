@@ -236,6 +236,12 @@ typedef struct ghx_arena ghx_arena;
 int ghx_arena_create(int32_t kind, int32_t memory, int32_t device, size_t capacity_bytes, ghx_arena **out);
 int ghx_arena_alloc(ghx_arena *a, size_t nbytes, size_t align, void **out);
 int ghx_arena_free(ghx_arena *a, void *ptr);
+/* Stream-ordered free: the block is recycled once the work queued so far on
+ * every given stream (cudaStream_t) has completed; nstreams == 0 frees now.
+ * Parked blocks still count as in use; ghx_arena_poll recycles the finished
+ * ones and reports how many are still parked. */
+int ghx_arena_free_after(ghx_arena *a, void *ptr, void *const *streams, int32_t nstreams);
+int ghx_arena_poll(ghx_arena *a, int64_t *parked);
 int ghx_arena_block_size(const ghx_arena *a, const void *ptr, size_t *padded);
 int ghx_arena_stats(const ghx_arena *a, int64_t out[4]);
 void ghx_arena_destroy(ghx_arena *a);

@@ -60,6 +60,8 @@ _SIGS = {
     "ghx_arena_create": (C.c_int, [I32, I32, I32, C.c_size_t, C.POINTER(P)]),
     "ghx_arena_alloc": (C.c_int, [P, C.c_size_t, C.c_size_t, C.POINTER(P)]),
     "ghx_arena_free": (C.c_int, [P, P]),
+    "ghx_arena_free_after": (C.c_int, [P, P, C.POINTER(P), I32]),
+    "ghx_arena_poll": (C.c_int, [P, PI64]),
     "ghx_arena_block_size": (C.c_int, [P, P, C.POINTER(C.c_size_t)]),
     "ghx_arena_stats": (C.c_int, [P, PI64]),
     "ghx_arena_destroy": (None, [P]),

@@ -7,8 +7,12 @@
 // kept on LIFO free lists segregated by (padded size, alignment) so repeated
 // temporaries never reach cudaMalloc; in_use counts alignment padding.  The
 // "system" kind makes one allocation per request (SystemArena,
-// arena.py:166-197).  Stream-ordered deferral of recycling (AsyncArena) is
-// done by the Python layer on top of this pool.
+// arena.py:166-197).  Stream-ordered reuse (the AsyncArena of arena.py:
+// 201-334 on a GPU): ghx_arena_free_after records an event on each stream
+// whose queued work may still touch the block and parks the block until
+// every event has completed; parked blocks are recycled by the next
+// alloc/free/poll that finds their events done (cudaFreeAsync-style
+// semantics, no host wait).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -82,6 +86,11 @@ struct ghx_arena {
   std::vector<Slab> slabs;
   std::map<std::pair<size_t, size_t>, std::vector<Blk>> free_lists;
   std::unordered_map<char *, Blk> live;
+  struct Parked {
+    Blk b;
+    std::vector<cudaEvent_t> events;
+  };
+  std::vector<Parked> parked;  // freed, waiting for stream work to finish
   int64_t reserved = 0, in_use = 0, alloc_calls = 0, slab_growths = 0;
 };
 
@@ -112,6 +121,43 @@ int carve(ghx_arena *a, size_t padded, size_t align, Blk *out) {
   s.cursor = start + padded;
   *out = Blk{s.base + start, padded, align, nullptr};
   return GHX_OK;
+}
+
+void release(ghx_arena *a, const Blk &b) {
+  a->in_use -= (int64_t)b.padded;
+  if (a->kind == GHX_ARENA_SYSTEM) {
+    a->reserved -= (int64_t)b.padded;
+    sys_free(a->memory, b.raw);
+  } else {
+    a->free_lists[{b.padded, b.align}].push_back(b);
+  }
+}
+
+// Recycle every parked block whose events have all completed (caller holds
+// a->mu).  Returns the number still parked.
+int64_t drain(ghx_arena *a) {
+  size_t keep = 0;
+  for (size_t i = 0; i < a->parked.size(); ++i) {
+    ghx_arena::Parked &p = a->parked[i];
+    bool done = true;
+    for (cudaEvent_t e : p.events) {
+      const cudaError_t q = cudaEventQuery(e);
+      if (q == cudaErrorNotReady) {
+        done = false;
+        break;
+      }
+      if (q != cudaSuccess) cudaGetLastError();  // a failed event cannot be waited on: treat as done
+    }
+    if (done) {
+      for (cudaEvent_t e : p.events) cudaEventDestroy(e);
+      release(a, p.b);
+    } else {
+      if (keep != i) a->parked[keep] = std::move(p);
+      ++keep;
+    }
+  }
+  a->parked.resize(keep);
+  return (int64_t)keep;
 }
 
 }  // namespace
@@ -154,6 +200,7 @@ int ghx_arena_alloc(ghx_arena *a, size_t nbytes, size_t align, void **out) {
   if (nbytes == 0) return GHX_OK;  // the null block
   const size_t padded = (nbytes + align - 1) / align * align;
   std::lock_guard<std::mutex> lk(a->mu);
+  if (!a->parked.empty()) drain(a);
   a->alloc_calls += 1;
   Blk b{};
   if (a->kind == GHX_ARENA_SYSTEM) {
@@ -193,13 +240,62 @@ int ghx_arena_free(ghx_arena *a, void *ptr) {
   }
   const Blk b = it->second;
   a->live.erase(it);
-  a->in_use -= (int64_t)b.padded;
-  if (a->kind == GHX_ARENA_SYSTEM) {
-    a->reserved -= (int64_t)b.padded;
-    sys_free(a->memory, b.raw);
-  } else {
-    a->free_lists[{b.padded, b.align}].push_back(b);
+  release(a, b);
+  if (!a->parked.empty()) drain(a);
+  return GHX_OK;
+}
+
+int ghx_arena_free_after(ghx_arena *a, void *ptr, void *const *streams, int32_t nstreams) {
+  if (!a || nstreams < 0 || (nstreams && !streams)) {
+    set_error("ghx_arena_free_after: bad arguments");
+    return GHX_EINVAL;
   }
+  if (!ptr) return GHX_OK;
+  std::lock_guard<std::mutex> lk(a->mu);
+  auto it = a->live.find(static_cast<char *>(ptr));
+  if (it == a->live.end()) {
+    set_error("ghx_arena_free_after: double free (or foreign pointer) of an arena block");
+    return GHX_EOVERLAP;
+  }
+  ghx_arena::Parked p{it->second, {}};
+  for (int32_t i = 0; i < nstreams; ++i) {
+    cudaStream_t st = static_cast<cudaStream_t>(streams[i]);
+    int dev = 0, prev = 0;
+    cudaGetDevice(&prev);
+    if (cudaStreamGetDevice(st, &dev) != cudaSuccess) {
+      cudaGetLastError();
+      dev = prev;
+    }
+    if (dev != prev) cudaSetDevice(dev);
+    cudaEvent_t e = nullptr;
+    cudaError_t rc = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    if (rc == cudaSuccess) rc = cudaEventRecord(e, st);
+    if (dev != prev) cudaSetDevice(prev);
+    if (rc != cudaSuccess) {
+      if (e) cudaEventDestroy(e);
+      for (cudaEvent_t x : p.events) cudaEventDestroy(x);
+      set_error(std::string("ghx_arena_free_after: ") + cudaGetErrorString(rc));
+      return GHX_ECUDA;
+    }
+    p.events.push_back(e);
+  }
+  a->live.erase(it);
+  if (p.events.empty())
+    release(a, p.b);
+  else
+    a->parked.push_back(std::move(p));
+  drain(a);
+  return GHX_OK;
+}
+
+int ghx_arena_poll(ghx_arena *a, int64_t *parked) {
+  if (!a) {
+    set_error("ghx_arena_poll: null arena");
+    return GHX_EINVAL;
+  }
+  std::lock_guard<std::mutex> lk(a->mu);
+  const int64_t n = drain(a);
+  if (parked) *parked = n;
   return GHX_OK;
 }
 
@@ -235,6 +331,13 @@ int ghx_arena_stats(const ghx_arena *a, int64_t out[4]) {
 
 void ghx_arena_destroy(ghx_arena *a) {
   if (!a) return;
+  for (auto &p : a->parked) {  // the slabs go away: let the queued work finish first
+    for (cudaEvent_t e : p.events) {
+      cudaEventSynchronize(e);
+      cudaEventDestroy(e);
+    }
+    if (p.b.raw) sys_free(a->memory, p.b.raw);
+  }
   for (auto &kv : a->live)
     if (kv.second.raw) sys_free(a->memory, kv.second.raw);
   for (auto &s : a->slabs) sys_free(a->memory, s.base);

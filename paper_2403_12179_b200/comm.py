@@ -512,20 +512,23 @@ class Executor:
 class Binding:
     """A pinned pointer table of an Executor (released with the object)."""
 
-    __slots__ = ("ex", "id", "_h", "__weakref__")
+    __slots__ = ("ex", "id", "__weakref__")
 
     def __init__(self, ex: Executor, bid: int):
         self.ex, self.id = ex, bid
-        self._h = ex._h
 
     def run(self, stream: int) -> None:
-        N.check(N.lib.ghx_exec_run_bound(self._h, self.id, C.c_void_p(stream)))
+        N.check(N.lib.ghx_exec_run_bound(self.ex._h, self.id, C.c_void_p(stream)))
 
     def __del__(self):
+        # the executor's live handle, never a cached copy: when a GC cycle
+        # holds both objects, Python may finalize the executor first
+        # (ghx_exec_free releases every binding with it)
         try:
-            if self.id:
-                N.lib.ghx_exec_unbind(self._h, self.id)
-                self.id = 0
+            h = self.ex._h
+            if self.id and h:
+                N.lib.ghx_exec_unbind(h, self.id)
+            self.id = 0
         except Exception:
             pass
 

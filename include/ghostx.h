@@ -192,6 +192,22 @@ int ghx_stream_sync(void *stream);
  * flag array (nranks uint64) as mapped in this process. */
 int ghx_signal_barrier(uint64_t *const *flag_ptrs, int32_t rank, int32_t nranks, uint64_t epoch,
                        void *stream);
+/* In-kernel synchronisation of process-mode exchanges (one GPU per rank),
+ * replacing the barrier -> push -> barrier -> unpack sequence: rank p's
+ * flag array holds 3*nranks uint64 slots ([0,n) ghx_signal_barrier, [n,2n)
+ * READY, [2n,3n) DONE).  ghx_exec_set_sync gives the executor every rank's
+ * array as mapped here.  ghx_exec_run_synced launches a push executor
+ * (DIRECT / PUSH_PACKED*) so that it signals READY to every peer on entry,
+ * runs its remote tasks (ordered first) only after the destination peer's
+ * READY, and signals DONE once all its pushes are visible; or a packed
+ * unpack executor so that each peer's receive slab is unpacked as soon as
+ * that peer's DONE lands and the kernel completes only after every peer's
+ * DONE.  ghx_exec_sync_wait is the DONE wait alone (direct mode exit).
+ * Epochs must increase and be identical on every rank. */
+int ghx_exec_set_sync(ghx_exec *ex, uint64_t *const *flag_arrays, int32_t rank, int32_t nranks);
+int ghx_exec_run_synced(ghx_exec *ex, int64_t binding, uint64_t epoch, void *stream);
+int ghx_exec_sync_wait(ghx_exec *ex, uint64_t epoch, void *stream);
+
 /* Number of device barriers (this process, current device) that gave up
  * after GHX_BARRIER_TIMEOUT_S seconds (default 30) instead of hanging;
  * synchronous read, -1 on error. */

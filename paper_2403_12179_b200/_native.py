@@ -57,6 +57,9 @@ _SIGS = {
     "ghx_exec_set_ring": (C.c_int, [P, I32]),
     "ghx_exec_task_kinds": (C.c_int, [P, PI64]),
     "ghx_exec_set_bulk": (C.c_int, [P, I32]),
+    "ghx_exec_set_sync": (C.c_int, [P, C.POINTER(P), I32, I32]),
+    "ghx_exec_run_synced": (C.c_int, [P, I64, C.c_uint64, P]),
+    "ghx_exec_sync_wait": (C.c_int, [P, C.c_uint64, P]),
     "ghx_arena_create": (C.c_int, [I32, I32, I32, C.c_size_t, C.POINTER(P)]),
     "ghx_arena_alloc": (C.c_int, [P, C.c_size_t, C.c_size_t, C.POINTER(P)]),
     "ghx_arena_free": (C.c_int, [P, P]),

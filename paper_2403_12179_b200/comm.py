@@ -31,6 +31,7 @@ from __future__ import annotations
 import ctypes as C
 import itertools
 import os
+import sys
 import threading
 import weakref
 from collections import deque
@@ -500,6 +501,15 @@ class Executor:
     def set_grid(self, blocks: int) -> None:
         N.check(N.lib.ghx_exec_set_grid(self._h, int(blocks), 256))
 
+    def set_sync(self, flag_table: np.ndarray, rank: int, nranks: int) -> None:
+        """In-kernel READY / DONE synchronisation over the ranks' IPC flag
+        arrays (ghx_exec_set_sync)."""
+        assert flag_table.dtype == np.uint64 and flag_table.size == nranks
+        N.check(N.lib.ghx_exec_set_sync(self._h, flag_table.ctypes.data_as(C.POINTER(C.c_void_p)), rank, nranks))
+
+    def sync_wait(self, epoch: int, stream: int) -> None:
+        N.check(N.lib.ghx_exec_sync_wait(self._h, C.c_uint64(epoch), C.c_void_p(stream)))
+
     def __del__(self):
         try:
             if self._h:
@@ -519,6 +529,9 @@ class Binding:
 
     def run(self, stream: int) -> None:
         N.check(N.lib.ghx_exec_run_bound(self.ex._h, self.id, C.c_void_p(stream)))
+
+    def run_synced(self, stream: int, epoch: int) -> None:
+        N.check(N.lib.ghx_exec_run_synced(self.ex._h, self.id, C.c_uint64(epoch), C.c_void_p(stream)))
 
     def __del__(self):
         # the executor's live handle, never a cached copy: when a GC cycle
@@ -653,8 +666,10 @@ class _ProcessSync:
     def __init__(self, ctx):
         self.ctx = ctx
         n = ctx.nranks
-        self.slab = Slab(8 * n, ctx.device)
-        N.check(N.lib.ghx_memset_u64(C.c_void_p(self.slab.ptr), 0, n, None))
+        # 3 * n slots: [0, n) barrier kernel, [n, 2n) READY, [2n, 3n) DONE
+        # (the in-kernel protocol of ghx_exec_run_synced)
+        self.slab = Slab(8 * 3 * n, ctx.device)
+        N.check(N.lib.ghx_memset_u64(C.c_void_p(self.slab.ptr), 0, 3 * n, None))
         import torch
         torch.cuda.synchronize(ctx.device)
         h = (C.c_uint8 * 64)()
@@ -672,6 +687,10 @@ class _ProcessSync:
             self._opened.append(p.value)
         self.table = np.asarray(self.ptrs, np.uint64)
         self.epoch = 0
+
+    def next_epoch(self) -> int:
+        self.epoch += 1
+        return self.epoch
 
     def barrier(self, stream: int) -> None:
         self.epoch += 1
@@ -800,6 +819,7 @@ class Exchange:
                 self.table = None  # thread ranks: gathered per call
         self._thread_bindings: dict = {}
         self._pin()
+        self._init_fused_sync()
         row = plan.pair_cells[me]
         self.messages = [(me, d, int(row[d]) * ncomp * self.item) for d in range(plan.nranks)
                          if d != me and row[d] > 0]
@@ -818,6 +838,20 @@ class Exchange:
             self._thread_bindings.pop(next(iter(self._thread_bindings)))
         b = self._thread_bindings[gen] = self.ex.bind(table, stream)
         return b
+
+    def _init_fused_sync(self) -> None:
+        """Device-sync process mode: the copy kernel itself waits for each
+        destination peer's READY and signals DONE; the unpack (or a DONE
+        wait) closes the exchange -- no standalone barrier kernels
+        (GHX_FUSED_SYNC=0 restores barrier -> push -> barrier -> unpack)."""
+        self.fused = (self.mode == "process" and self.sync == "device" and self.transport == "p2p"
+                      and os.environ.get("GHX_FUSED_SYNC", "1") != "0")
+        if not self.fused:
+            return
+        ps = self.psync
+        self.ex.set_sync(ps.table, self.ctx.rank, self.ctx.nranks)
+        if self.unp is not None:
+            self.unp.set_sync(ps.table, self.ctx.rank, self.ctx.nranks)
 
     def _pin(self) -> None:
         """Pin every pointer table this exchange launches with (once)."""
@@ -959,6 +993,13 @@ class Exchange:
             self._enqueue_nccl(stream)
         elif self.mode == "serial":
             self.b_ex.run(stream)
+        elif self.mode == "process" and self.sync == "device" and self.fused:
+            e = self.psync.next_epoch()
+            self.b_ex.run_synced(stream, e)  # pushes wait per peer for READY, then signal DONE
+            if self.unp is not None:
+                self.b_unp.run_synced(stream, e)  # each peer's slab unpacked once its DONE lands
+            else:
+                self.ex.sync_wait(e, stream)  # every push into my fabs has landed
         elif self.mode == "process" and self.sync == "device":
             self.psync.barrier(stream)  # peers finished earlier work on their fabs
             self.b_ex.run(stream)
@@ -1081,17 +1122,69 @@ def prepare_parallel_copy(dst: MultiFab, src: MultiFab, scomp: int = 0, dcomp: i
 
 # --------------------------------------------------------------- public entry
 
+def _raw_stream_fn():
+    import torch
+    f = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    return f if f is not None else (lambda dev: torch.cuda.current_stream(dev).cuda_stream)
+
+
+_raw_stream = None
+
+
+def _dist_initialized() -> bool:
+    d = sys.modules.get("torch.distributed")
+    return d is not None and d.is_available() and d.is_initialized()
+
+
+def _plan_key_of(mf: MultiFab, plan) -> object:
+    for k, v in mf.plan_cache.items():
+        if v is plan:
+            return k
+    return None
+
+
+def _fill_boundary_serial_fast(mf: MultiFab, geom, backend) -> bool:
+    """Repeat call of a single-rank FillBoundary: one bound launch and one
+    stream synchronize, no plan lookup or Python object churn (the first
+    call took the full path and left ``mf._fb_fast``).  False = take the
+    full path."""
+    fast = getattr(mf, "_fb_fast", None)
+    if fast is None or backend is not None or geom is not fast[0]:
+        return False
+    if getattr(_tls, "ctx", None) is not None or _dist_initialized() or mf.plan_cache.get(fast[2]) is not fast[3]:
+        return False
+    h, bid, dev = fast[1].ex._h, fast[1].id, mf.device
+    if not h:
+        return False
+    st = _raw_stream(dev)
+    rc = N.lib.ghx_exec_run_bound(h, bid, C.c_void_p(st))
+    if rc == 0:
+        rc = N.lib.ghx_stream_sync(C.c_void_p(st))
+    N.check(rc)
+    return True
+
+
 def fill_boundary(mf: MultiFab, geom: Geometry | None = None, backend=None) -> None:
     """Fill every coverable ghost cell of ``mf`` from (periodically shifted)
     valid data.  Collective over ranks; at most one message per ordered rank
     pair; physical-boundary ghosts with no source and all valid cells are
     left untouched (reference comm.py:383-394)."""
+    if _fill_boundary_serial_fast(mf, geom, backend):
+        return
     plan = plan_build_fill_boundary(mf, geom)
     if plan.is_empty:
         return
     ctx = current_ctx()
     _execute_plan(plan, mf, mf, 0, 0, mf.ncomp, ctx, backend)
     ctx.barrier()
+    if ctx is _serial_ctx:
+        ex = exchange_for(plan, mf, mf, 0, 0, mf.ncomp, ctx)
+        if ex.mode == "serial" and ex.transport == "p2p" and getattr(ex, "b_ex", None) is not None:
+            global _raw_stream
+            if _raw_stream is None:
+                _raw_stream = _raw_stream_fn()
+            # the geometry object this plan was built for (None = mf.geom)
+            mf._fb_fast = (geom, ex.b_ex, _plan_key_of(mf, plan), plan)
 
 
 def _pc_args(dst, src, scomp, dcomp, ncomp, ngrow_src, ngrow_dst):

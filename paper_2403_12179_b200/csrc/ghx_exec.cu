@@ -461,7 +461,87 @@ __device__ __forceinline__ void fetch_tag(const DevTag *__restrict__ tags, int i
     reinterpret_cast<uint4 *>(slot)[lane] = __ldg(reinterpret_cast<const uint4 *>(tags + idx) + lane);
 }
 
+// In-kernel cross-rank synchronisation (process mode, one GPU per rank).
+// Every rank owns an IPC-shared flag array of 3 * nranks uint64 slots:
+// [0, n) the standalone barrier kernel's, [n, 2n) READY (rank p has started
+// this exchange, so its earlier work on its fabs and receive slab is done),
+// [2n, 3n) DONE (every store rank p pushed to me in this exchange is
+// visible).  Values are the exchange epoch, monotonic and identical on all
+// ranks, so a slot never needs resetting.
+//   mode 1 (push kernel): each block's warp 0 signals READY to every peer on
+//     entry; the remote tasks -- the first `nhead` tasks -- wait for their
+//     peer's READY (once per warp per peer) while local tasks start at
+//     once; the last warp to finish fences and signals DONE to every peer.
+//   mode 2 (unpack kernel): a task reading peer p's receive slab waits for
+//     p's DONE (each peer's slab is unpacked as soon as it lands), and block
+//     0 waits for every peer's DONE (direct pushes into my fabs) before the
+//     kernel can complete.
+// Spins give up after timeout_ns and count a timeout (ghx_barrier_timeouts)
+// instead of hanging the GPU when a peer rank dies.
+constexpr int kSlotReady = 1, kSlotDone = 2;
+
+struct SyncArgs {
+  uint64_t *const *flags;   // device table: rank p's flag array as mapped here
+  const int32_t *tag_peer;  // per tag: peer rank (push: destination, unpack: source), -1 local
+  uint64_t epoch;
+  uint64_t timeout_ns;
+  int32_t rank, nranks;
+  int32_t mode;             // 0 none, 1 push, 2 unpack / wait
+  int32_t nhead;            // mode 1: tasks [0, nhead) are remote
+};
+
+__device__ unsigned int g_sync_timeouts = 0;
+
+__device__ __forceinline__ uint64_t gtimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void flag_store(uint64_t *p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __noinline__ void flag_wait(const uint64_t *p, uint64_t epoch, uint64_t timeout_ns) {
+  const uint64_t t0 = gtimer_ns();
+  uint64_t v = 0;
+  for (uint32_t it = 0;; ++it) {
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    if (v >= epoch) return;
+    if ((it & 1023) == 1023 && gtimer_ns() - t0 > timeout_ns) {
+      atomicAdd(&g_sync_timeouts, 1u);
+      return;
+    }
+    __nanosleep(64);
+  }
+}
+
+// every peer's slot `slot` of this rank's flag array reaches the epoch
+__device__ __forceinline__ void wait_all_peers(const SyncArgs &s, int slot, int lane) {
+  for (int p = lane; p < s.nranks; p += 32)
+    if (p != s.rank) flag_wait(s.flags[s.rank] + slot * s.nranks + p, s.epoch, s.timeout_ns);
+}
+
+__device__ __forceinline__ void signal_all_peers(const SyncArgs &s, int slot, int lane) {
+  for (int p = lane; p < s.nranks; p += 32)
+    if (p != s.rank) flag_store(s.flags[p] + slot * s.nranks + s.rank, s.epoch);
+}
+
 }  // namespace
+
+// Empty executors still take part in the protocol: mode 1 signals READY
+// and DONE, mode 2 waits for every peer's DONE (direct-mode exit wait).
+__global__ void ghx_sync_kernel(const SyncArgs sync) {
+  const int lane = threadIdx.x;
+  if (lane >= 32) return;
+  if (sync.mode == 1) {
+    __threadfence_system();
+    signal_all_peers(sync, kSlotReady, lane);
+    signal_all_peers(sync, kSlotDone, lane);
+  } else if (sync.mode == 2) {
+    wait_all_peers(sync, kSlotDone, lane);
+  }
+}
 
 // Resolve pointer-table slots into absolute addresses (once per table).
 __global__ void ghx_bind_kernel(DevTag *tags, int ntags, void *const *__restrict__ ptrs) {
@@ -481,7 +561,8 @@ template <int LD, bool RING = false, bool BULK = false>
 __global__ void __launch_bounds__(kThreads, GHX_MINB) ghx_copy_kernel(const DevTag *__restrict__ tags,
                                                             const int4 *__restrict__ tasks, int ntasks,
                                                             const int *__restrict__ chains,
-                                                            unsigned long long *__restrict__ counter, int batch) {
+                                                            unsigned long long *__restrict__ counter, int batch,
+                                                            const SyncArgs sync) {
   __shared__ DevTag slots[kWarps][2];
   __shared__ DevTag swc[kWarps][kSwapSlots];  // direct-mapped cache of sector-swap descriptors
   __shared__ int swc_id[kWarps][kSwapSlots];
@@ -501,6 +582,8 @@ __global__ void __launch_bounds__(kThreads, GHX_MINB) ghx_copy_kernel(const DevT
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
   }
+  if (sync.mode == 1 && wib == 0) signal_all_peers(sync, kSlotReady, lane);
+  uint64_t peers_ok = 0;  // peers whose READY (mode 1) / DONE (mode 2) this warp has seen
   __syncwarp();
   // first batch static (warp id), later ones dynamic from an offset of one
   // batch per warp: no atomic -- and no contention of every warp on one
@@ -517,6 +600,17 @@ __global__ void __launch_bounds__(kThreads, GHX_MINB) ghx_copy_kernel(const DevT
 #pragma unroll 1
     for (int w = (int)first; w < last; ++w) {
       const int4 nxt = (w + 1 < last) ? __ldg(tasks + w + 1) : tk;
+      if (tk.z >= -1 && (sync.mode == 2 || (sync.mode == 1 && w < sync.nhead))) {
+        // a remote push waits for the peer's READY, an unpack for its DONE
+        const int peer = __ldg(sync.tag_peer + tk.x);
+        if (peer >= 0 && peer < 64 && !((peers_ok >> peer) & 1ull)) {
+          if (lane == 0)
+            flag_wait(sync.flags[sync.rank] + (sync.mode == 1 ? kSlotReady : kSlotDone) * sync.nranks + peer,
+                      sync.epoch, sync.timeout_ns);
+          __syncwarp();
+          peers_ok |= 1ull << peer;
+        }
+      }
       if (tk.z == -3) {  // chain task: all seams of one chain, kChainRows rows
         chain_task<LD>(tags, chains, tk.x, tk.w, (uint32_t)tk.y, kChainRows, lane);
       } else if (RING && tk.z == -4) {  // ring task: seam chunks of 32/(2k) columns of one x-ring
@@ -566,9 +660,17 @@ __global__ void __launch_bounds__(kThreads, GHX_MINB) ghx_copy_kernel(const DevT
     nb = __shfl_sync(0xffffffffu, nb, 0);
   }
   if (BULK) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // this lane's bulk stores are done
+  if (sync.mode == 2 && blockIdx.x == 0 && wib == 0) wait_all_peers(sync, kSlotDone, lane);
+  if (sync.mode == 1) __threadfence_system();  // this lane's pushes are visible system-wide
+  __syncwarp();
   if (lane == 0) {
     const unsigned long long total = (unsigned long long)gridDim.x * (blockDim.x >> 5);
     if (atomicAdd(counter + 1, 1ull) == total - 1) {
+      if (sync.mode == 1) {  // every warp has fenced its pushes: tell the peers
+        __threadfence_system();
+        for (int p = 0; p < sync.nranks; ++p)
+          if (p != sync.rank) flag_store(sync.flags[p] + kSlotDone * sync.nranks + sync.rank, sync.epoch);
+      }
       counter[0] = 0;
       counter[1] = 0;
     }
@@ -619,6 +721,7 @@ struct HostTag {
   Side s, d;
   int64_t nx, ny, nz, nc;  // elements
   bool remote;
+  int32_t peer;            // push: destination rank of a remote tag; unpack: source rank; else -1
   int32_t sfab, dfab;      // plan fab ids (pairing)
   int64_t shift[3];
 };
@@ -660,6 +763,12 @@ struct ghx_exec {
   std::vector<DevTag> htags;
   std::vector<PairKey> hkeys;
   std::vector<int32_t> hremote;
+  std::vector<int32_t> hpeer;   // per tag (SyncArgs::tag_peer)
+  int32_t nhead = 0;            // remote tasks at the head of htasks
+  // in-kernel synchronisation (ghx_exec_set_sync)
+  int32_t sync_rank = -1, sync_n = 0;
+  uint64_t **dflags = nullptr;
+  int32_t *dpeer = nullptr;
   std::vector<int4> htasks;
   std::vector<int> hchain;  // chain tables (tag indices of consecutive seams)
   int *dchain = nullptr;
@@ -722,6 +831,7 @@ void add_devtag(ghx_exec *ex, const HostTag &t, int64_t x0, int64_t nxe, int vl,
   ex->htags.push_back(g);
   ex->hkeys.emplace_back(t.sfab, t.dfab, t.shift[0], t.shift[1], t.shift[2], part, g.nxv, g.ny, g.nz, vl);
   ex->hremote.push_back(t.remote ? 1 : 0);
+  ex->hpeer.push_back(t.peer);
 }
 
 // Split a row range into an unaligned head, 16-byte body and tail when src
@@ -968,10 +1078,23 @@ void build_tasks(ghx_exec *ex) {
     }
     if (!swaps.empty()) loc.swap(merged);
   }
-  // proportional interleave of local (HBM) and remote (NVLink) work
+  // remote (NVLink) tasks first, so the pushes -- the longer pole at N > 1
+  // -- start at t = 0 and the local HBM work fills in behind them
+  // (GHX_REMOTE_ORDER=interleave: the earlier proportional interleave)
   std::vector<int4> &a = loc;
   const std::vector<int4> &b = rem;
-  if (!b.empty()) {
+  static const bool interleave = [] {
+    const char *v = std::getenv("GHX_REMOTE_ORDER");
+    return v && std::string(v) == "interleave";
+  }();
+  ex->nhead = 0;
+  if (!b.empty() && !interleave) {
+    std::vector<int4> merged(b);
+    merged.insert(merged.end(), a.begin(), a.end());
+    a.swap(merged);
+    ex->nhead = (int32_t)b.size();
+  } else if (!b.empty()) {
+    ex->nhead = (int32_t)(a.size() + b.size());  // remote tasks anywhere: every task checks its peer
     std::vector<int4> merged;
     merged.reserve(a.size() + b.size());
     size_t ia = 0, ib = 0;
@@ -995,7 +1118,7 @@ void build_tasks(ghx_exec *ex) {
       const int64_t per_comp = std::max<int64_t>(1, (int64_t)d.nxv * d.ny * d.nz);
       return {std::get<1>(ex->hkeys[tag]), (int64_t)t.y / per_comp, (int64_t)t.y % per_comp};
     };
-    std::stable_sort(a.begin(), a.end(), [&](const int4 &l, const int4 &r) { return key(l) < key(r); });
+    std::stable_sort(a.begin() + (interleave ? 0 : ex->nhead), a.end(), [&](const int4 &l, const int4 &r) { return key(l) < key(r); });
   }
   ex->htasks.swap(a);
 }
@@ -1094,6 +1217,7 @@ int ghx_exec_create(const ghx_plan *plan, int32_t rank, int32_t kind, const int6
     t.nz = p.dbox.hi[2] - p.dbox.lo[2] + 1;
     t.nc = ncomp;
     t.remote = p.srank != p.drank;
+    t.peer = !t.remote ? -1 : (src_is_fab ? p.drank : p.srank);
     t.sfab = p.src;
     t.dfab = p.dst;
     for (int d = 0; d < 3; ++d) t.shift[d] = p.shift[d];
@@ -1244,6 +1368,8 @@ void ghx_exec_free(ghx_exec *ex) {
   if (ex->dtasks) cudaFree(ex->dtasks);
   if (ex->dchain) cudaFree(ex->dchain);
   if (ex->dptrs) cudaFree(ex->dptrs);
+  if (ex->dflags) cudaFree(ex->dflags);
+  if (ex->dpeer) cudaFree(ex->dpeer);
   delete ex;
 }
 
@@ -1429,7 +1555,7 @@ int find_or_bind(ghx_exec *ex, void *const *ptrs, int64_t nptrs, cudaStream_t st
   return GHX_OK;
 }
 
-int launch(ghx_exec *ex, ghx_exec::Binding *bd, cudaStream_t st) {
+int launch(ghx_exec *ex, ghx_exec::Binding *bd, cudaStream_t st, const SyncArgs &sync) {
   bd->last_use = ++ex->uses;
   DevTag *const dtags = bd->dtags;
   unsigned long long *const counter = bd->counter;
@@ -1450,15 +1576,15 @@ int launch(ghx_exec *ex, ghx_exec::Binding *bd, cudaStream_t st) {
     // attribute: set it once on every device that launches bulk rows
     if (int rc = bulk_smem_attr(ex->device)) return rc;
     ghx_copy_kernel<2, false, true><<<ex->blocks, ex->threads, kWarps * kBulkBytes, st>>>(
-        dtags, ex->dtasks, ntasks, ex->dchain, counter, batch);
+        dtags, ex->dtasks, ntasks, ex->dchain, counter, batch, sync);
   } else if (ex->nring) {  // ring tasks present: the ring-capable instantiation
-    ghx_copy_kernel<2, true><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, counter, batch);
+    ghx_copy_kernel<2, true><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, counter, batch, sync);
   } else switch (ld) {
-    case 0: ghx_copy_kernel<0><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, counter, batch); break;
-    case 1: ghx_copy_kernel<1><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, counter, batch); break;
-    case 2: ghx_copy_kernel<2><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, counter, batch); break;
-    case 3: ghx_copy_kernel<3><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, counter, batch); break;
-    default: ghx_copy_kernel<4><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, counter, batch); break;
+    case 0: ghx_copy_kernel<0><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, counter, batch, sync); break;
+    case 1: ghx_copy_kernel<1><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, counter, batch, sync); break;
+    case 2: ghx_copy_kernel<2><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, counter, batch, sync); break;
+    case 3: ghx_copy_kernel<3><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, counter, batch, sync); break;
+    default: ghx_copy_kernel<4><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, counter, batch, sync); break;
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "ghx_exec_run: launch");
@@ -1482,7 +1608,7 @@ int ghx_exec_run(ghx_exec *ex, void *const *ptrs, int64_t nptrs, void *stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   ghx_exec::Binding *bd = nullptr;
   if (int rc = find_or_bind(ex, ptrs, nptrs, st, &bd)) return rc;
-  return launch(ex, bd, st);
+  return launch(ex, bd, st, SyncArgs{});
 }
 
 int ghx_exec_bind(ghx_exec *ex, void *const *ptrs, int64_t nptrs, void *stream, int64_t *binding) {
@@ -1521,9 +1647,103 @@ int ghx_exec_run_bound(ghx_exec *ex, int64_t binding, void *stream) {
   std::lock_guard<std::mutex> lk(ex->mu);
   DeviceGuard g(ex->device);
   for (auto &b : ex->bindings)
-    if (b->id == binding && b->pins > 0) return launch(ex, b.get(), static_cast<cudaStream_t>(stream));
+    if (b->id == binding && b->pins > 0) return launch(ex, b.get(), static_cast<cudaStream_t>(stream), SyncArgs{});
   set_error("ghx_exec_run_bound: unknown or released binding " + std::to_string(binding));
   return GHX_EINVAL;
+}
+
+static uint64_t sync_timeout_ns() {
+  static const uint64_t ns = [] {
+    const char *v = std::getenv("GHX_BARRIER_TIMEOUT_S");
+    const double sec = v ? std::atof(v) : 30.0;
+    return (uint64_t)(sec * 1e9);
+  }();
+  return ns;
+}
+
+int ghx_exec_set_sync(ghx_exec *ex, uint64_t *const *flag_arrays, int32_t rank, int32_t nranks) {
+  if (!ex || !flag_arrays || nranks < 1 || nranks > 64 || rank < 0 || rank >= nranks || nranks != ex->nranks) {
+    set_error("ghx_exec_set_sync: bad arguments (nranks <= 64, matching the plan)");
+    return GHX_EINVAL;
+  }
+  for (int i = 0; i < nranks; ++i)
+    if (!flag_arrays[i]) {
+      set_error("ghx_exec_set_sync: null flag array");
+      return GHX_EINVAL;
+    }
+  std::lock_guard<std::mutex> lk(ex->mu);
+  DeviceGuard g(ex->device);
+  cudaError_t e = cudaSuccess;
+  if (!ex->dflags) e = cudaMalloc(&ex->dflags, 64 * sizeof(uint64_t *));
+  if (e == cudaSuccess) e = cudaMemcpy(ex->dflags, flag_arrays, nranks * sizeof(uint64_t *), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && !ex->dpeer)
+    e = cudaMalloc(&ex->dpeer, std::max<size_t>(1, ex->hpeer.size()) * sizeof(int32_t));
+  if (e == cudaSuccess && !ex->hpeer.empty())
+    e = cudaMemcpy(ex->dpeer, ex->hpeer.data(), ex->hpeer.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail(e, "ghx_exec_set_sync");
+  ex->sync_rank = rank;
+  ex->sync_n = nranks;
+  return GHX_OK;
+}
+
+static int sync_args(ghx_exec *ex, uint64_t epoch, int32_t mode, SyncArgs *out) {
+  if (ex->sync_rank < 0 || !ex->dflags) {
+    set_error("ghx_exec_run_synced: ghx_exec_set_sync was not called");
+    return GHX_EINVAL;
+  }
+  SyncArgs s{};
+  s.flags = ex->dflags;
+  s.tag_peer = ex->dpeer;
+  s.epoch = epoch;
+  s.timeout_ns = sync_timeout_ns();
+  s.rank = ex->sync_rank;
+  s.nranks = ex->sync_n;
+  s.mode = mode;
+  s.nhead = ex->nhead;
+  *out = s;
+  return GHX_OK;
+}
+
+int ghx_exec_run_synced(ghx_exec *ex, int64_t binding, uint64_t epoch, void *stream) {
+  if (!ex) {
+    set_error("ghx_exec_run_synced: null handle");
+    return GHX_EINVAL;
+  }
+  const bool unpack = ex->kind == GHX_EXEC_UNPACK_PACKED || ex->kind == GHX_EXEC_UNPACK_PACKED_ALL;
+  const bool push = ex->kind == GHX_EXEC_DIRECT || ex->kind == GHX_EXEC_PUSH_PACKED ||
+                    ex->kind == GHX_EXEC_PUSH_PACKED_ALL;
+  if (!unpack && !push) {
+    set_error("ghx_exec_run_synced: only push (direct / packed) and packed-unpack executors synchronise in-kernel");
+    return GHX_EINVAL;
+  }
+  std::lock_guard<std::mutex> lk(ex->mu);
+  DeviceGuard g(ex->device);
+  SyncArgs s;
+  if (int rc = sync_args(ex, epoch, unpack ? 2 : 1, &s)) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (ex->htasks.empty()) {  // nothing to move: still signal (push) / wait (unpack)
+    ghx_sync_kernel<<<1, 32, 0, st>>>(s);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? GHX_OK : cuda_fail(e, "ghx_exec_run_synced: sync kernel");
+  }
+  for (auto &b : ex->bindings)
+    if (b->id == binding && b->pins > 0) return launch(ex, b.get(), st, s);
+  set_error("ghx_exec_run_synced: unknown or released binding " + std::to_string(binding));
+  return GHX_EINVAL;
+}
+
+int ghx_exec_sync_wait(ghx_exec *ex, uint64_t epoch, void *stream) {
+  if (!ex) {
+    set_error("ghx_exec_sync_wait: null handle");
+    return GHX_EINVAL;
+  }
+  std::lock_guard<std::mutex> lk(ex->mu);
+  DeviceGuard g(ex->device);
+  SyncArgs s;
+  if (int rc = sync_args(ex, epoch, 2, &s)) return rc;
+  ghx_sync_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(s);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? GHX_OK : cuda_fail(e, "ghx_exec_sync_wait");
 }
 
 int ghx_exec_unbind(ghx_exec *ex, int64_t binding) {
@@ -1543,3 +1763,10 @@ int ghx_exec_unbind(ghx_exec *ex, int64_t binding) {
 }
 
 }  // extern "C"
+
+// timeouts of the in-kernel waits (added to ghx_barrier_timeouts)
+int64_t ghx::sync_timeouts() {
+  unsigned int v = 0;
+  if (cudaMemcpyFromSymbol(&v, g_sync_timeouts, sizeof(v)) != cudaSuccess) return -1;
+  return (int64_t)v;
+}

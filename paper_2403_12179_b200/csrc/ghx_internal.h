@@ -65,4 +65,5 @@ struct ghx_plan {
 
 namespace ghx {
 void set_error(const std::string &msg);
+int64_t sync_timeouts();  // ghx_exec.cu: in-kernel READY/DONE waits that gave up
 }

@@ -356,7 +356,8 @@ static int fill_hash(void *fab, const int64_t fab_box[6], int32_t ncomp, const i
 int64_t ghx_barrier_timeouts(void) {
   unsigned int v = 0;
   if (cudaMemcpyFromSymbol(&v, g_barrier_timeouts, sizeof(v)) != cudaSuccess) return -1;
-  return (int64_t)v;
+  const int64_t k = ghx::sync_timeouts();
+  return k < 0 ? -1 : (int64_t)v + k;
 }
 
 int ghx_fill_hash(void *fab, const int64_t fab_box[6], int32_t ncomp, const int64_t valid_box[6],

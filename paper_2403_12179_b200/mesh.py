@@ -399,6 +399,7 @@ class MultiFab:
         self.plan_cache: dict = {}
         self.plan_builds = 0
         self._peer_cache: dict = {}
+        self._fb_fast = None  # comm.fill_boundary's single-rank repeat-call entry
         self._alloc()
 
     def _alloc(self) -> None:
@@ -463,6 +464,7 @@ class MultiFab:
         self._slab = None
         self._ptrs = np.zeros(0, np.uint64)
         self._peer_cache = {}  # cached executors hold device pointers into the released storage
+        self._fb_fast = None
         self._closed = True
 
     def check_open(self) -> None:

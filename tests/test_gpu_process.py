@@ -73,8 +73,16 @@ def _worker(rank, world, port, q, n, b, nc, ng, env=None):
 
 CASES = [("C1", 64, 32, 1, 1, "C1_x2", {"GHX_REMOTE": "direct"}), ("C3", 512, 128, 8, 2, "C3_x2", {}),
          ("C3", 512, 128, 8, 2, "C3_x2", {"GHX_REMOTE": "direct"}),
-         # device flag barriers between two processes time-sliced on one GPU
+         # device flag barriers between two processes time-sliced on one GPU:
+         # the in-kernel READY / DONE protocol (default), packed and direct,
+         # and the standalone barrier kernels (GHX_FUSED_SYNC=0)
          ("C1", 64, 32, 1, 1, "C1_x2", {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "20"}),
+         ("C1", 64, 32, 1, 1, "C1_x2", {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "20", "GHX_REMOTE": "direct"}),
+         ("C3", 512, 128, 8, 2, "C3_x2", {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "20"}),
+         ("C3", 512, 128, 8, 2, "C3_x2", {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "20", "GHX_REMOTE": "direct"}),
+         ("C1", 64, 32, 1, 1, "C1_x2", {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "20", "GHX_FUSED_SYNC": "0"}),
+         ("C1", 64, 32, 1, 1, "C1_x2", {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "20",
+                                        "GHX_REMOTE_ORDER": "interleave"}),
          # the pack -> message -> unpack fallback (host-staged over gloo here)
          ("C1", 64, 32, 1, 1, "C1_x2", {"GHX_TRANSPORT": "nccl"}),
          ("C3", 512, 128, 8, 2, "C3_x2", {"GHX_TRANSPORT": "nccl"}),
@@ -86,7 +94,8 @@ CASES = [("C1", 64, 32, 1, 1, "C1_x2", {"GHX_REMOTE": "direct"}), ("C3", 512, 12
 
 
 @pytest.mark.parametrize("cfg", CASES, ids=["C1-ipc-direct", "C3-ipc-packed", "C3-ipc-direct", "C1-devbarrier-packed",
-                                            "C1-fallback", "C3-fallback", "C1-arena-ipc", "C1-pinned",
+                                            "C1-devsync-direct", "C3-devsync-packed", "C3-devsync-direct",
+                                            "C1-devbarrier-unfused", "C1-devsync-interleave", "C1-fallback", "C3-fallback", "C1-arena-ipc", "C1-pinned",
                                             "C3-pinned"])
 def test_two_processes_one_gpu(cfg):
     _run(cfg, 2)
@@ -95,8 +104,10 @@ def test_two_processes_one_gpu(cfg):
 # C3 at 4 and 8 ranks (8 and 40 ordered pairs): every rank maps
 # every peer it pushes to; message accounting against the reference's plan
 @pytest.mark.parametrize("world,env", [(4, {}), (4, {"GHX_TRANSPORT": "nccl"}), (8, {}),
-                                       (4, {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "30"})],
-                         ids=["C3x4-ipc-packed", "C3x4-fallback", "C3x8-ipc-packed", "C3x4-devbarrier"])
+                                       (4, {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "30"}),
+                                       (4, {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "30", "GHX_REMOTE": "direct"})],
+                         ids=["C3x4-ipc-packed", "C3x4-fallback", "C3x8-ipc-packed", "C3x4-devbarrier",
+                              "C3x4-devsync-direct"])
 def test_many_processes_one_gpu(world, env):
     _run(("C3", 512, 128, 8, 2, f"C3_x{world}", env), world)
 

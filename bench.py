@@ -669,6 +669,9 @@ def run_ours(args, cfg, rank, world):
         best = max(best, 2 * big.numel() * 2 / (e0.elapsed_time(e1) * 1e-3) / 1e9)
     del big, big2
     alg = x.ex.alg_bytes if x.transport == "p2p" else None
+    split = None
+    if world == 1 and cfg["kind"] == "fb" and isinstance(cfg["ngrow"], int) and not args.no_split:
+        split = direction_split(amr, cfg, L, stream, flush, clean, mean_ms)
     roof = None
     if alg is not None:
         achieved = alg / (mean_ms * 1e-3) / 1e9
@@ -685,6 +688,8 @@ def run_ours(args, cfg, rank, world):
             floor_ms = tmin / (hbm_peak * 1e9) * 1e3
             hbm["modelled_floor_ms"] = round(floor_ms, 5)
             hbm["frac_of_modelled_floor"] = round(floor_ms / mean_ms, 4)
+        if split is not None:
+            hbm["direction_split"] = split
         roof = hbm
         if world > 1:
             pc = x.plan.pair_cells.astype(np.float64) * x.ncomp * x.item
@@ -763,6 +768,49 @@ def run_ours(args, cfg, rank, world):
         print(json.dumps(line), flush=True)
 
 
+def direction_split(amr, cfg, L, stream, flush, clean, all_ms, reps=20):
+    """The same FillBoundary split by direction, measured in this run: the
+    x faces alone (ngrow (g,0,0): the same x-row seams at the same row
+    pitch) and the y/z faces alone (ngrow (0,g,g)), each device-timed like
+    the headline.  x_only + yz_only is the additive floor the fused kernel
+    is compared with: the x-row seams cost one DRAM
+    line read + one line write each whatever their size, and they compete
+    with the face rows for the same DRAM service."""
+    import torch
+    from paper_2403_12179_b200 import comm
+    g = cfg["ngrow"]
+    out = {}
+    for name, ng in (("x_only", (g, 0, 0)), ("yz_only", (0, g, g))):
+        mf = amr.MultiFab(L["ba"], L["dm"], cfg["ncomp"], amr.IntVect(*ng), L["geom"])
+        mf.fill_hash(SEED, L["dom"])
+        xx = comm.exchange_for(comm.plan_build_fill_boundary(mf, L["geom"]), mf, mf, 0, 0, mf.ncomp)
+        for _ in range(3):
+            xx.enqueue(stream.cuda_stream)
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            if clean is not None:
+                torch.sum(clean)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            xx.enqueue(stream.cuda_stream)
+            e1.record(stream)
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        out[name + "_ms"] = round(sum(ts) / len(ts), 5)
+        if name == "x_only":
+            rows = sum(int((b.hi[1] - b.lo[1] + 1) * (b.hi[2] - b.lo[2] + 1)) for b in L["ba"]) * cfg["ncomp"]
+            out["x_row_seams"] = rows
+            out["x_gseam_per_s"] = round(rows / (out["x_only_ms"] * 1e-3) / 1e9, 2)
+        del xx, mf
+        torch.cuda.synchronize()
+    add = out["x_only_ms"] + out["yz_only_ms"]
+    out["additive_floor_ms"] = round(add, 5)
+    out["all_ms"] = round(all_ms, 5)
+    out["frac_of_additive_floor"] = round(add / all_ms, 4)
+    return out
+
+
 def e2e_leg(args, amr, cfg, L, world, ghost_bytes, x):
     """The public call on MultiFabs in pinned host memory (zero-copy: the
     exchange kernels read source cells and write ghost cells across PCIe).
@@ -828,6 +876,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-split", action="store_true", help="skip the x / y-z direction split (N=1)")
     ap.add_argument("--no-port", action="store_true", help="skip the numpy-port sample next to the reference")
     ap.add_argument("--ngrow", default=None, help="diagnostic: override ghost width per axis, e.g. 2,0,0")
     args = ap.parse_args()

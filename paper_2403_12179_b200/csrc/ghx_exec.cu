@@ -177,16 +177,29 @@ __device__ __forceinline__ int64_t vec_offset(const DevTag &t, uint32_t v) {
              : (int64_t)x + (int64_t)y * t.dst_sy + (int64_t)z * t.dst_sz + (int64_t)c * t.dst_sc;
 }
 
-template <int LD>
+#ifndef GHX_HOST_CONT
+#define GHX_HOST_CONT 0  // experiment knob (scripts/build_variants.sh); measured slower, see DESIGN.md
+#endif
+// CONT (fabs in host memory): an isolated 16-byte row (edge / corner tags,
+// one vector per row) is read as its aligned 32-byte sector -- over PCIe a
+// 16-byte read costs twice a 32-byte one (profiles/r01_pcie_probe.txt:
+// 0.28 vs 0.57 G requests/s); the sector never crosses a page, and the
+// other half is discarded.
+template <int LD, bool CONT = false>
 __device__ __forceinline__ void load_chunk(const DevTag &t, uint32_t start, int lane, uint4 (&val)[kU]) {
   const char *base = reinterpret_cast<const char *>(t.src);
   const int vl = t.vlog;
+  const bool cont = CONT && vl == 4 && t.nxv == 1;
 #pragma unroll
   for (int u = 0; u < kU; ++u) {
     const uint32_t v = start + (uint32_t)(u * 32 + lane);
     if (v < t.nvec) {
       const char *p = base + (vec_offset<true>(t, v) << vl);
-      if (vl == 4)
+      if (cont) {
+        const u8x32 s = ld32<LD>(reinterpret_cast<const char *>(reinterpret_cast<uintptr_t>(p) & ~uintptr_t(31)));
+        val[u] = (reinterpret_cast<uintptr_t>(p) & 16) ? make_uint4(s.w[4], s.w[5], s.w[6], s.w[7])
+                                                       : make_uint4(s.w[0], s.w[1], s.w[2], s.w[3]);
+      } else if (vl == 4)
         val[u] = ld16<LD>(p);
       else if (vl == 3) {
         const uint2 q = ld8<LD>(p);
@@ -400,6 +413,96 @@ __device__ __forceinline__ void ring_task(const DevTag *__restrict__ tags, const
   }
 }
 
+// Tile ring task: the same seam chunks, but one warp instruction covers k
+// fabs x R = 16/k CONSECUTIVE chunks of one (z, comp) column, and the warp
+// steps down R chunks at a time (ring_task covers k fabs x 16/k columns, one
+// chunk each).  Over PCIe the host side serves a warp's requests faster when
+// they fall on neighbouring rows (scripts/microbench/pcie_ring_probe.cu:
+// 4.0 ns per seam read+write against 4.3 for the column layout; the seam
+// read of the next step is issued before this step's write).
+// Chunk c of fab j = [S0 row c | S1 row c+1]; its new contents are
+//   q0 = S0(j,c).lo (kept)        q1 = S1(j+1,c).hi = chunk(j+1,c-1).q3
+//   q2 = S0(j-1,c+1).lo = chunk(j-1,c+1).q0        q3 = S1(j,c+1).hi (kept)
+// Lane (j, r, side) holds chunk c = c0 + t*R + r of fab j at step t (side 0
+// the S0 sector, side 1 the S1 sector).  q1 comes from lane (j+1, r-1, 1)
+// this step, or for r = 0 from lane (j+1, R-1, 1)'s previous step; q2 from
+// lane (j-1, r+1, 0) this step, or for r = R-1 from lane (j-1, 0, 0)'s next
+// step (already loaded as the prefetch): one shuffle per step, every lane
+// offering exactly the half some other lane needs.  A task owns chunks
+// [c0, c0 + nch) of its column; chunks run from -1 (S1 row 0 only) to ny-1
+// (S0 row ny-1 only), and only sectors of rows in [0, ny) are touched.
+template <int LD>
+__device__ __forceinline__ void tile_ring_task(const DevTag *__restrict__ tags, const int *__restrict__ ring, int off,
+                                               int q, int kw, int lane) {
+  const int k = kw & 31;
+  const int c0 = ((kw >> 5) & 0xFFFF) - 1;
+  const int span = (kw >> 21) & 0x1FF;  // chunks owned: [c0, c0 + span)
+  const int R = 16 / k;
+  const int steps = (span + R - 1) / R;
+  const int p = lane >> 1, side = lane & 1;
+  const int j = p % k, r = p / k;
+  const bool active = r < R;
+  const int jn = (j + 1) % k, jp = (j + k - 1) % k;
+  const DevTag &t = tags[__ldg(ring + off + (side ? jp : j))];
+  const char *base = reinterpret_cast<const char *>(side ? __ldg(&t.dst) : __ldg(&t.src));
+  const int64_t sy = side ? __ldg(&t.dst_sy) : __ldg(&t.src_sy);
+  const int64_t sz = side ? __ldg(&t.dst_sz) : __ldg(&t.src_sz);
+  const int64_t sc = side ? __ldg(&t.dst_sc) : __ldg(&t.src_sc);
+  const int ny = (int)__ldg(&t.ny), nz = (int)__ldg(&t.nz);
+  const char *col = base + ((((int64_t)(q % nz)) * sz + (int64_t)(q / max(nz, 1)) * sc) << 4);
+  const int c_end = min(c0 + span, ny);  // chunks run -1 .. ny-1
+  // the row of my sector in chunk c: side 0 -> row c (S0), side 1 -> row c + 1 (S1)
+  auto row_of = [&](int c) { return side ? c + 1 : c; };
+  auto ok = [&](int c) { const int y = row_of(c); return active && y >= 0 && y < ny; };
+  auto addr = [&](int c) { return const_cast<char *>(col + (((int64_t)row_of(c) * sy) << 4)); };
+  // source lanes of the one shuffle per step
+  const int src = side ? 2 * (jp + k * ((r + 1) % R)) : 2 * (jn + k * ((r + R - 1) % R)) + 1;
+  u8x32 cur, nxt;
+  uint4 prev_hi = make_uint4(0, 0, 0, 0);
+  // halo: lane (j, R-1, 1) starts with chunk c0-1's S1 high half (q3) for lane (jp, 0, 0)
+  if (side && r == R - 1 && ok(c0 - 1)) {
+    const u8x32 h = ld32<LD>(addr(c0 - 1));
+    prev_hi = make_uint4(h.w[4], h.w[5], h.w[6], h.w[7]);
+  }
+  {
+    const int c = c0 + r;
+    if (ok(c)) cur = ld32<LD>(addr(c));
+  }
+#pragma unroll 1
+  for (int s = 0; s < steps; ++s) {
+    const int c = c0 + s * R + r;
+    const int cn = c + R;
+    // next step's sector (lane (j, 0, 0) also serves the last step's halo)
+    if (ok(cn) && (s + 1 < steps || (r == 0 && !side))) nxt = ld32<LD>(addr(cn));
+    // what I offer: side 0 my q0 (or, at r = 0, the next step's q0); side 1
+    // my q3 (or, at r = R-1, the previous step's q3)
+    uint4 give;
+    if (side)
+      give = (r == R - 1) ? prev_hi : make_uint4(cur.w[4], cur.w[5], cur.w[6], cur.w[7]);
+    else
+      give = (r == 0) ? make_uint4(nxt.w[0], nxt.w[1], nxt.w[2], nxt.w[3])
+                      : make_uint4(cur.w[0], cur.w[1], cur.w[2], cur.w[3]);
+    uint4 got;
+    got.x = __shfl_sync(0xffffffffu, give.x, src);
+    got.y = __shfl_sync(0xffffffffu, give.y, src);
+    got.z = __shfl_sync(0xffffffffu, give.z, src);
+    got.w = __shfl_sync(0xffffffffu, give.w, src);
+    if (ok(c) && c < c_end) {
+      uint32_t w[8];
+      if (side) {
+        w[0] = got.x, w[1] = got.y, w[2] = got.z, w[3] = got.w;
+        w[4] = cur.w[4], w[5] = cur.w[5], w[6] = cur.w[6], w[7] = cur.w[7];
+      } else {
+        w[0] = cur.w[0], w[1] = cur.w[1], w[2] = cur.w[2], w[3] = cur.w[3];
+        w[4] = got.x, w[5] = got.y, w[6] = got.z, w[7] = got.w;
+      }
+      st32(addr(c), w);
+    }
+    if (side && r == R - 1) prev_hi = make_uint4(cur.w[4], cur.w[5], cur.w[6], cur.w[7]);
+    cur = nxt;
+  }
+}
+
 // Bulk-row task (TMA 1-D bulk copies): rows of a 16-byte-vector tag are
 // moved global -> shared -> global by the copy engine of the SM, one lane
 // per row (cp.async.bulk with an mbarrier per warp), so a warp keeps
@@ -558,7 +661,7 @@ __global__ void ghx_bind_kernel(DevTag *tags, int ntags, void *const *__restrict
 // counter[1] and the last one resets both, so the next launch (stream
 // ordered) starts from zero without a memset.  Heavy tasks come first.
 template <int LD, bool RING = false, bool BULK = false>
-__global__ void __launch_bounds__(kThreads, GHX_MINB) ghx_copy_kernel(const DevTag *__restrict__ tags,
+__global__ void __launch_bounds__(kThreads, RING ? 1 : GHX_MINB) ghx_copy_kernel(const DevTag *__restrict__ tags,
                                                             const int4 *__restrict__ tasks, int ntasks,
                                                             const int *__restrict__ chains,
                                                             unsigned long long *__restrict__ counter, int batch,
@@ -615,6 +718,8 @@ __global__ void __launch_bounds__(kThreads, GHX_MINB) ghx_copy_kernel(const DevT
         chain_task<LD>(tags, chains, tk.x, tk.w, (uint32_t)tk.y, kChainRows, lane);
       } else if (RING && tk.z == -4) {  // ring task: seam chunks of 32/(2k) columns of one x-ring
         ring_task<LD>(tags, chains, tk.x, tk.w, tk.y, lane);
+      } else if (RING && tk.z == -6) {  // tile ring task: k fabs x 16/k consecutive seam chunks per step
+        tile_ring_task<LD>(tags, chains, tk.x, tk.y, tk.w, lane);
       } else if (BULK && tk.z == -5) {  // bulk-row task: tk.w rows of tag tk.x from row tk.y
         if (tk.x != have_a || have_b != -5) {
           __syncwarp();
@@ -650,8 +755,8 @@ __global__ void __launch_bounds__(kThreads, GHX_MINB) ghx_copy_kernel(const DevT
           __syncwarp();
         }
         uint4 va[kU], vb[kU];
-        load_chunk<LD>(ta, (uint32_t)tk.y, lane, va);
-        if (tk.z >= 0) load_chunk<LD>(tb, (uint32_t)tk.w, lane, vb);
+        load_chunk<LD, RING && GHX_HOST_CONT>(ta, (uint32_t)tk.y, lane, va);
+        if (tk.z >= 0) load_chunk<LD, RING && GHX_HOST_CONT>(tb, (uint32_t)tk.w, lane, vb);
         store_chunk(ta, (uint32_t)tk.y, lane, va);
         if (tk.z >= 0) store_chunk(tb, (uint32_t)tk.w, lane, vb);
       }
@@ -1017,6 +1122,11 @@ void build_tasks(ghx_exec *ex) {
     for (int32_t t : swap_lo) chains[find(std::get<0>(ex->hkeys[t]))].push_back(t);
     const bool chain_tasks = std::getenv("GHX_NO_CHAIN") == nullptr && !ex->fab_local;
     const bool ring_mode = ex->ring;
+    // tile ring tasks (default) or the column-layout ring tasks (GHX_RING_TILE=0)
+    static const bool tile_ring = [] {
+      const char *v = std::getenv("GHX_RING_TILE");
+      return !v || std::atoi(v) != 0;
+    }();
     for (auto &kv : chains) {
       std::vector<int32_t> &ts = kv.second;
       std::sort(ts.begin(), ts.end());
@@ -1032,6 +1142,22 @@ void build_tasks(ghx_exec *ex) {
           const int off = (int)ex->hchain.size();
           ex->hchain.insert(ex->hchain.end(), order.begin(), order.end());
           ex->nring += 2 * k;
+          if (tile_ring && t0.ny + 1 <= 65534) {
+            // tile ring tasks: one column each, chunk ranges of ~32
+            // (balanced), columns in address order
+            const int R = 16 / k;
+            const uint32_t nch = t0.ny + 1;
+            const uint32_t per_task = (uint32_t)std::max(R, 8 * R);
+            const uint32_t nt = (nch + per_task - 1) / per_task;
+            const uint32_t span = (nch + nt - 1) / nt;
+            for (uint32_t q = 0; q < ncols; ++q)
+              for (uint32_t a = 0; a < nch; a += span) {
+                const uint32_t sp = std::min(span, nch - a);
+                // c0 + 1 = a (chunk -1 is a = 0)
+                swaps.push_back(make_int4(off, (int)q, -6, k | (int)(a << 5) | (int)(sp << 21)));
+              }
+            continue;
+          }
           // column-major (q, then row segment): concurrent warps stay on few
           // host pages (fabs in host memory are the ring's use)
           const uint32_t nseg = (t0.ny + kRingRows - 1) / kRingRows;
@@ -1059,9 +1185,10 @@ void build_tasks(ghx_exec *ex) {
     if (std::getenv("GHX_BULK_FIRST")) {  // experiment: bulk face rows first, then the seams
       loc.insert(loc.end(), swaps.begin(), swaps.end());
       swaps.clear();
-    } else if (std::getenv("GHX_NO_INTERLEAVE") || ex->nbulk) {
+    } else if (std::getenv("GHX_NO_INTERLEAVE") || ex->nbulk || ex->ring) {
       // bulk (TMA) face rows and latency-bound seams interfere when
-      // interleaved (measured); seams first, then the bulk rows
+      // interleaved (measured); seams first, then the bulk rows.  Same over
+      // PCIe (host-memory fabs, ring tasks): C3 e2e 56.3 -> 53.8 ms
       swaps.insert(swaps.end(), loc.begin(), loc.end());
       loc.swap(swaps);
       swaps.clear();
@@ -1113,7 +1240,7 @@ void build_tasks(ghx_exec *ex) {
     // hit in L2 (C4: -23 % time, C2: -6 %; measured)
     // key: (destination fab, component, position in the component)
     auto key = [&](const int4 &t) -> std::tuple<int64_t, int64_t, int64_t> {
-      const int32_t tag = (t.z == -4 || t.z == -3) ? ex->hchain[t.x] : t.x;
+      const int32_t tag = (t.z == -4 || t.z == -3 || t.z == -6) ? ex->hchain[t.x] : t.x;
       const DevTag &d = ex->htags[tag];
       const int64_t per_comp = std::max<int64_t>(1, (int64_t)d.nxv * d.ny * d.nz);
       return {std::get<1>(ex->hkeys[tag]), (int64_t)t.y / per_comp, (int64_t)t.y % per_comp};
@@ -1451,7 +1578,7 @@ int ghx_exec_task_kinds(const ghx_exec *ex, int64_t out[6]) {
   }
   for (int i = 0; i < 6; ++i) out[i] = 0;
   for (const int4 &t : ex->htasks) {
-    if (t.z == -4)
+    if (t.z == -4 || t.z == -6)
       out[3] += 1;
     else if (t.z == -3)
       out[2] += 1;

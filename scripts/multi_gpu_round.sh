@@ -1,8 +1,10 @@
 #!/usr/bin/env bash
 # Multi-GPU measurement pass for a box with N >= 2 B200s (one process per
-# GPU, NCCL plumbing): weak-scaled C2, the north-star C3 and the C5 regrid at 2/4/8 GPUs
-# over the CUDA-IPC push (packed and direct remote rows, device barriers) and
-# the NCCL pack/send/unpack fallback.
+# GPU, NCCL plumbing): the north-star C3 first (BASELINE configs[2], the
+# bench default), then C5 and C2, at 2/4/8 GPUs over the CUDA-IPC push
+# (packed and direct remote rows; in-kernel READY/DONE sync, plus the
+# standalone-barrier sequence GHX_FUSED_SYNC=0 for comparison) and the NCCL
+# pack/send/unpack fallback.
 # Output: gpurun_out/multi/<config>_<transport>_<N>.json (one bench line each).
 #   bash scripts/multi_gpu_round.sh [max_gpus]
 set -u
@@ -11,11 +13,11 @@ export PYTHONDONTWRITEBYTECODE=1
 MAXG=${1:-$(nvidia-smi -L | wc -l)}
 nvidia-smi topo -m > gpurun_out/multi/topo.txt 2>&1
 port=29600
-for cfg in C2 C3 C5; do
+for cfg in C3 C5 C2; do
   steps=100; [ "$cfg" = C5 ] && steps=20
   for n in 2 4 8; do
     [ "$n" -le "$MAXG" ] || continue
-    for variant in "p2p:GHX_REMOTE=packed" "p2p:GHX_REMOTE=direct" "nccl:GHX_TRANSPORT=nccl"; do
+    for variant in "p2p:GHX_REMOTE=packed" "p2p:GHX_REMOTE=direct" "p2pbar:GHX_FUSED_SYNC=0" "nccl:GHX_TRANSPORT=nccl"; do
       tag=${variant%%:*}; envs=${variant#*:}
       port=$((port + 1))
       env $envs GHX_BARRIER_TIMEOUT_S=30 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n \

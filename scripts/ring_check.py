@@ -10,11 +10,14 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_2403_12179_b200 as amr  # noqa: E402
+
+_bad_total = 0
 from gpu_util import device_bits, expected_wrapped  # noqa: E402
 
 amr.config.set_spacedim(3)
 for (nx, ny, nz, b, nc) in [(128, 64, 64, 64, 1), (192, 64, 64, 64, 1), (256, 64, 64, 64, 1), (64, 64, 64, 64, 1),
-                            (128, 128, 128, 64, 2), (128, 32, 32, 32, 1)]:
+                            (128, 128, 128, 64, 2), (128, 32, 32, 32, 1), (96, 40, 24, 32, 1),
+                            (256, 32, 48, 32, 2), (512, 32, 32, 32, 1), (64, 200, 16, 64, 1)]:
     dom = amr.Box((0, 0, 0), (nx - 1, ny - 1, nz - 1))
     geom = amr.Geometry(dom, (0.0,) * 3, (1.0,) * 3, (True,) * 3)
     ba = amr.decompose(dom, b)
@@ -29,3 +32,5 @@ for (nx, ny, nz, b, nc) in [(128, 64, 64, 64, 1), (192, 64, 64, 64, 1), (256, 64
         bad += int((device_bits(f) != exp).sum().item())
     print(nx, ny, nz, b, nc, "ring tasks", ex.detail["ring_tasks"], "swap", ex.detail["swap_tasks"], "bad", bad,
           flush=True)
+    _bad_total += bad
+sys.exit(1 if _bad_total else 0)

@@ -49,8 +49,11 @@ def test_small_fabs_use_fab_ordered_swaps(n, b):
 def test_ring_tasks_for_periodic_xlines():
     k = kinds(256, 64, 4, 2, ring=True)
     assert k["ring_mode"] == 1 and k["ring"] > 0 and k["swap"] == 0 and k["chain"] == 0
-    # 16 x-lines of 4 fabs, 4 streams of (z, comp) columns per task, 64 rows in 16-row segments
-    assert k["ring"] == 16 * (64 * 4 // 4) * (64 // 16)
+    # tile ring tasks: 16 x-lines of 4 fabs, one task per (z, comp) column and
+    # balanced range of the 65 seam chunks (rows -1 .. 63): at most 8 steps of
+    # 16/4 = 4 chunks -> 3 tasks of 22 / 22 / 21 chunks per column
+    nch, per = 64 + 1, 8 * (16 // 4)
+    assert k["ring"] == 16 * (64 * 4) * (-(-nch // per))
 
 
 def test_open_xlines_fall_back_to_swaps():

@@ -61,6 +61,15 @@ extern "C" {
  * its own host fabs. */
 #define GHX_EXEC_PUSH_PACKED_ALL 6
 #define GHX_EXEC_UNPACK_PACKED_ALL 7
+/* OR into the kind of a DIRECT / LOCAL FillBoundary executor whose tags are
+ * all local: run the exchange in three phases (x faces; y faces extended over
+ * the x ghosts; z faces extended over the x and y ghosts, reading the source
+ * fab's ghosts filled by the earlier phases) with no edge / corner tags.
+ * Same result bit for bit (fabs whose tags do not allow it keep theirs);
+ * fewer, longer rows -- meant for fabs in host memory, where each PCIe
+ * request costs.  Warps wait for each other between phases, so the grid
+ * must be co-resident (host executors run 8 CTAs). */
+#define GHX_EXEC_PHASED 0x100
 
 typedef struct ghx_plan ghx_plan;
 typedef struct ghx_exec ghx_exec;
@@ -167,6 +176,10 @@ int ghx_exec_set_bulk(ghx_exec *ex, int32_t on);
 /* Task mix: out[6] = copy tasks, sector-swap tasks, x-line chain tasks,
  * seam-chunk ring tasks, ring mode on, fab-local order on. */
 int ghx_exec_task_kinds(const ghx_exec *ex, int64_t out[6]);
+
+/* Phased executors: out[4] = phased (0/1), first task of phase 1, first task
+ * of phase 2, device tags. */
+int ghx_exec_phases(const ghx_exec *ex, int64_t out[4]);
 
 /* Launch-time tuning knob (warps per block * blocks): 0 = default. */
 int ghx_exec_set_grid(ghx_exec *ex, int32_t blocks, int32_t threads);

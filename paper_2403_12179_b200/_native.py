@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("GHX_LIB") or os.path.join(_HERE, "_lib", "libghostx.s
 GHX_OK, GHX_EINVAL, GHX_ECUDA, GHX_ENOMEM, GHX_EOVERLAP = 0, 1, 2, 3, 4
 MODE_FILL_BOUNDARY, MODE_PARALLEL_COPY = 0, 1
 EXEC_DIRECT, EXEC_LOCAL, EXEC_PACK, EXEC_UNPACK, EXEC_PUSH_PACKED, EXEC_UNPACK_PACKED = 0, 1, 2, 3, 4, 5
+EXEC_PHASED = 0x100  # flag OR-ed into the kind (include/ghostx.h)
 EXEC_PUSH_PACKED_ALL, EXEC_UNPACK_PACKED_ALL = 6, 7
 
 P = C.c_void_p
@@ -58,6 +59,7 @@ _SIGS = {
     "ghx_exec_task_kinds": (C.c_int, [P, PI64]),
     "ghx_exec_set_bulk": (C.c_int, [P, I32]),
     "ghx_exec_set_sync": (C.c_int, [P, C.POINTER(P), I32, I32]),
+    "ghx_exec_phases": (C.c_int, [P, PI64]),
     "ghx_exec_run_synced": (C.c_int, [P, I64, C.c_uint64, P]),
     "ghx_exec_sync_wait": (C.c_int, [P, C.c_uint64, P]),
     "ghx_arena_create": (C.c_int, [I32, I32, I32, C.c_size_t, C.POINTER(P)]),

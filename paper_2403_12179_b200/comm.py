@@ -419,14 +419,19 @@ class CommPlan:
         # distinct source and destination storage: no byte is read after being
         # written in one run, so wide rows may go through TMA bulk copies
         bulk = src_mf is not dst_mf and not host and os.environ.get("GHX_PC_BULK", "1") == "1"
+        # fabs in host memory: the phased exchange (faces extended over the
+        # lower-axis ghosts, no edge / corner tags: fewer PCIe requests);
+        # GHX_PHASED=1 / 0 forces it on / off (device fabs: parity testing)
+        phased = kind in (N.EXEC_DIRECT, N.EXEC_LOCAL) and src_mf is dst_mf and \
+            {"1": True, "0": False}.get(os.environ.get("GHX_PHASED", ""), host)
         key = (rank, kind, src_mf.ngrow.comps, src_mf.ncomp, dst_mf.ngrow.comps, dst_mf.ncomp,
-               scomp, dcomp, ncomp, dst_mf.dtype.itemsize, dst_mf.device, ring, host, bulk)
+               scomp, dcomp, ncomp, dst_mf.dtype.itemsize, dst_mf.device, ring, host, bulk, phased)
         with self._lock:
             ex = self._execs.get(key)
             if ex is None:
-                ex = Executor(self, rank, kind, src_mf.storage_rows(), src_mf.ncomp, dst_mf.storage_rows(),
-                              dst_mf.ncomp, scomp, dcomp, ncomp, dst_mf.dtype.itemsize, dst_mf.device, ring, host,
-                              bulk)
+                ex = Executor(self, rank, kind | (N.EXEC_PHASED if phased else 0), src_mf.storage_rows(),
+                              src_mf.ncomp, dst_mf.storage_rows(), dst_mf.ncomp, scomp, dcomp, ncomp,
+                              dst_mf.dtype.itemsize, dst_mf.device, ring, host, bulk)
                 self._execs[key] = ex
         return ex
 
@@ -479,6 +484,9 @@ class Executor:
         N.check(N.lib.ghx_exec_task_kinds(h, N.i64p(kinds)))
         self.detail.update(zip(("copy_tasks", "swap_tasks", "chain_tasks", "ring_tasks", "ring_mode", "fab_local"),
                                (int(v) for v in kinds)))
+        ph = np.zeros(4, np.int64)
+        N.check(N.lib.ghx_exec_phases(h, N.i64p(ph)))
+        self.detail["phased"] = int(ph[0])
 
     def run(self, table: np.ndarray, stream: int) -> None:
         """One launch with a raw pointer table (bound on the fly; an

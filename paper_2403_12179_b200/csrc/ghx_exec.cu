@@ -431,6 +431,9 @@ __device__ __forceinline__ void ring_task(const DevTag *__restrict__ tags, const
 // offering exactly the half some other lane needs.  A task owns chunks
 // [c0, c0 + nch) of its column; chunks run from -1 (S1 row 0 only) to ny-1
 // (S0 row ny-1 only), and only sectors of rows in [0, ny) are touched.
+#ifndef GHX_RING_W16
+#define GHX_RING_W16 0
+#endif
 template <int LD>
 __device__ __forceinline__ void tile_ring_task(const DevTag *__restrict__ tags, const int *__restrict__ ring, int off,
                                                int q, int kw, int lane) {
@@ -488,6 +491,13 @@ __device__ __forceinline__ void tile_ring_task(const DevTag *__restrict__ tags, 
     got.z = __shfl_sync(0xffffffffu, give.z, src);
     got.w = __shfl_sync(0xffffffffu, give.w, src);
     if (ok(c) && c < c_end) {
+#if GHX_RING_W16
+      // only the ghost half: the pair's two 16-B stores are the 32 adjacent
+      // ghost bytes of the seam (one PCIe write, the kept halves untouched)
+      char *g = addr(c) + (side ? 0 : 16);
+      asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(g), "r"(got.x), "r"(got.y), "r"(got.z), "r"(got.w)
+                   : "memory");
+#else
       uint32_t w[8];
       if (side) {
         w[0] = got.x, w[1] = got.y, w[2] = got.z, w[3] = got.w;
@@ -497,6 +507,7 @@ __device__ __forceinline__ void tile_ring_task(const DevTag *__restrict__ tags, 
         w[4] = got.x, w[5] = got.y, w[6] = got.z, w[7] = got.w;
       }
       st32(addr(c), w);
+#endif
     }
     if (side && r == R - 1) prev_hi = make_uint4(cur.w[4], cur.w[5], cur.w[6], cur.w[7]);
     cur = nxt;
@@ -591,6 +602,7 @@ struct SyncArgs {
   int32_t rank, nranks;
   int32_t mode;             // 0 none, 1 push, 2 unpack / wait
   int32_t nhead;            // mode 1: tasks [0, nhead) are remote
+  int32_t pe0, pe1;         // phased executor: tasks [pe0, pe1) phase 1, [pe1, n) phase 2 (0, 0: no phases)
 };
 
 __device__ unsigned int g_sync_timeouts = 0;
@@ -687,6 +699,32 @@ __global__ void __launch_bounds__(kThreads, RING ? 1 : GHX_MINB) ghx_copy_kernel
   }
   if (sync.mode == 1 && wib == 0) signal_all_peers(sync, kSlotReady, lane);
   uint64_t peers_ok = 0;  // peers whose READY (mode 1) / DONE (mode 2) this warp has seen
+  // phased executor: a warp passing into phase p (it grabbed a task of phase
+  // p, so it will run no task of an earlier phase again) counts itself in
+  // counter[2 + p - 1] and waits until every warp has; tasks are grabbed in
+  // index order, so every waiter waits only for warps still running tasks
+  const bool phased = sync.pe1 > 0 || sync.pe0 > 0;
+  int my_phase = 0;
+  const unsigned long long nwarps_all = (unsigned long long)gridDim.x * kWarps;
+  auto pass_to = [&](int ph, bool wait) {
+    while (my_phase < ph) {
+      __syncwarp();
+      __threadfence_system();  // my earlier phases' stores (host memory too) are visible
+      __syncwarp();
+      if (lane == 0) atomicAdd(counter + 2 + my_phase, 1ull);
+      ++my_phase;
+      if (wait) {
+        if (lane == 0) {
+          unsigned long long v = 0;
+          do {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(counter + 2 + my_phase - 1) : "memory");
+            if (v < nwarps_all) __nanosleep(128);
+          } while (v < nwarps_all);
+        }
+        __syncwarp();
+      }
+    }
+  };
   __syncwarp();
   // first batch static (warp id), later ones dynamic from an offset of one
   // batch per warp: no atomic -- and no contention of every warp on one
@@ -703,6 +741,7 @@ __global__ void __launch_bounds__(kThreads, RING ? 1 : GHX_MINB) ghx_copy_kernel
 #pragma unroll 1
     for (int w = (int)first; w < last; ++w) {
       const int4 nxt = (w + 1 < last) ? __ldg(tasks + w + 1) : tk;
+      if (phased) pass_to(w >= sync.pe1 ? 2 : (w >= sync.pe0 ? 1 : 0), true);
       if (tk.z >= -1 && (sync.mode == 2 || (sync.mode == 1 && w < sync.nhead))) {
         // a remote push waits for the peer's READY, an unpack for its DONE
         const int peer = __ldg(sync.tag_peer + tk.x);
@@ -765,6 +804,7 @@ __global__ void __launch_bounds__(kThreads, RING ? 1 : GHX_MINB) ghx_copy_kernel
     nb = __shfl_sync(0xffffffffu, nb, 0);
   }
   if (BULK) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // this lane's bulk stores are done
+  if (phased) pass_to(3, false);  // no more tasks: count out of every remaining phase
   if (sync.mode == 2 && blockIdx.x == 0 && wib == 0) wait_all_peers(sync, kSlotDone, lane);
   if (sync.mode == 1) __threadfence_system();  // this lane's pushes are visible system-wide
   __syncwarp();
@@ -778,6 +818,9 @@ __global__ void __launch_bounds__(kThreads, RING ? 1 : GHX_MINB) ghx_copy_kernel
       }
       counter[0] = 0;
       counter[1] = 0;
+      counter[2] = 0;
+      counter[3] = 0;
+      counter[4] = 0;
     }
   }
 }
@@ -844,6 +887,126 @@ int vec_log(const HostTag &t, int64_t eb, int64_t x0, int64_t nxe) {
   return eb == 8 ? 3 : 2;
 }
 
+// Phased FillBoundary (GHX_EXEC_PHASED, fabs in host memory): every face
+// tag that reaches its destination's valid boundary in a lower axis is
+// extended over the destination's ghost cells in that axis, reading the
+// source fab's own ghost cells there -- which the earlier phases have filled
+// with the same periodic images the edge and corner tags would have read.
+// The edge / corner tags inside the extensions are dropped, so over PCIe a
+// ghost row is one request instead of a row plus two 16-byte pieces.
+// Why the values agree: a ghost cell g of A is filled by the reference iff
+// its periodically wrapped position is covered by a valid box, and then
+// with that cell's value; the extension reads S's cell g - shift, whose
+// wrapped position is the same (shifts are period multiples), and which is
+// either valid or a ghost cell of S in lower axes only (filled by an earlier
+// phase iff covered).  Per destination fab the transformation is kept only
+// if the extensions exactly tile the dropped tags (same cells), are
+// disjoint from everything else, and read inside the source storage;
+// otherwise that fab keeps its original tags (any layout stays bit-exact).
+// Returns false if the plan does not qualify at all (nothing changed).
+bool phase_pieces(const ghx_plan *plan, int32_t rank, const std::vector<Box> &sstore, std::vector<Piece> &ps,
+                  std::vector<int8_t> &phase) {
+  if (plan->mode != GHX_MODE_FILL_BOUNDARY || plan->clipped || (int64_t)plan->vbox.size() != plan->ndst) return false;
+  const size_t n = ps.size();
+  std::vector<int> gmask(n, 0);
+  for (size_t i = 0; i < n; ++i) {
+    const Piece &p = ps[i];
+    if (p.srank != rank || p.drank != rank) return false;
+    const Box &V = plan->vbox[p.dst];
+    for (int d = 0; d < 3; ++d) {
+      if (p.dbox.hi[d] < V.lo[d] || p.dbox.lo[d] > V.hi[d])
+        gmask[i] |= 1 << d;
+      else if (p.dbox.lo[d] < V.lo[d] || p.dbox.hi[d] > V.hi[d])
+        return false;  // straddles the valid boundary
+    }
+    if (!gmask[i]) return false;  // writes valid cells (not a cell-centred exchange)
+    phase[i] = (int8_t)(gmask[i] & 4 ? 2 : gmask[i] & 2 ? 1 : 0);
+  }
+  std::vector<std::vector<size_t>> by_dst(plan->ndst);
+  for (size_t i = 0; i < n; ++i) by_dst[ps[i].dst].push_back(i);
+  std::vector<uint8_t> drop(n, 0);
+  std::vector<Box> ext(n);
+  for (size_t i = 0; i < n; ++i) ext[i] = ps[i].dbox;
+  auto cells = [](const Box &b) { return b.cells(); };
+  auto inside = [](const Box &in, const Box &out) {
+    for (int d = 0; d < 3; ++d)
+      if (in.lo[d] < out.lo[d] || in.hi[d] > out.hi[d]) return false;
+    return true;
+  };
+  for (int32_t a = 0; a < plan->ndst; ++a) {
+    const std::vector<size_t> &ids = by_dst[a];
+    const Box &V = plan->vbox[a];
+    std::vector<Box> e(ids.size());
+    std::vector<uint8_t> isface(ids.size(), 0), extended(ids.size(), 0), rm(ids.size(), 0);
+    bool ok = true;
+    int64_t ext_cells = 0;
+    for (size_t u = 0; u < ids.size(); ++u) {
+      const Piece &p = ps[ids[u]];
+      e[u] = p.dbox;
+      const int g = gmask[ids[u]];
+      if (g & (g - 1)) continue;  // edge / corner
+      isface[u] = 1;
+      const int d = g == 1 ? 0 : g == 2 ? 1 : 2;
+      for (int x = 0; x < d; ++x) {
+        if (plan->ngrow[x] <= 0) continue;
+        if (p.dbox.lo[x] == V.lo[x]) e[u].lo[x] = V.lo[x] - plan->ngrow[x];
+        if (p.dbox.hi[x] == V.hi[x]) e[u].hi[x] = V.hi[x] + plan->ngrow[x];
+      }
+      if (cells(e[u]) != cells(p.dbox)) {
+        extended[u] = 1;
+        ext_cells += cells(e[u]) - cells(p.dbox);
+        Box sb = e[u];
+        for (int d2 = 0; d2 < 3; ++d2) {
+          sb.lo[d2] -= p.shift[d2];
+          sb.hi[d2] -= p.shift[d2];
+        }
+        if (!inside(sb, sstore[p.src])) ok = false;
+      }
+    }
+    // every edge / corner tag lies inside one extension or outside all
+    int64_t rm_cells = 0;
+    for (size_t u = 0; u < ids.size() && ok; ++u) {
+      if (isface[u]) continue;
+      int in = 0, touch = 0;
+      for (size_t w = 0; w < ids.size(); ++w) {
+        if (!extended[w]) continue;
+        if (inside(ps[ids[u]].dbox, e[w])) ++in;
+        else if (ghx::overlap(ps[ids[u]].dbox, e[w])) ++touch;
+      }
+      if (touch || in > 1) ok = false;
+      if (in == 1) {
+        rm[u] = 1;
+        rm_cells += cells(ps[ids[u]].dbox);
+      }
+    }
+    // extensions disjoint from each other and from every kept tag
+    for (size_t u = 0; u < ids.size() && ok; ++u) {
+      if (!extended[u]) continue;
+      for (size_t w = 0; w < ids.size() && ok; ++w) {
+        if (w == u || rm[w]) continue;
+        if (ghx::overlap(e[u], extended[w] ? e[w] : ps[ids[w]].dbox)) ok = false;
+      }
+    }
+    if (!ok || rm_cells != ext_cells) continue;  // this fab keeps its original tags
+    for (size_t u = 0; u < ids.size(); ++u) {
+      if (rm[u]) drop[ids[u]] = 1;
+      if (extended[u]) ext[ids[u]] = e[u];
+    }
+  }
+  std::vector<Piece> out;
+  std::vector<int8_t> ph;
+  for (size_t i = 0; i < n; ++i) {
+    if (drop[i]) continue;
+    Piece p = ps[i];
+    p.dbox = ext[i];
+    out.push_back(p);
+    ph.push_back(phase[i]);
+  }
+  ps.swap(out);
+  phase.swap(ph);
+  return true;
+}
+
 // pairing key of a device tag: (src fab, dst fab, shift, part, shape)
 using PairKey = std::tuple<int32_t, int32_t, int64_t, int64_t, int64_t, int, uint32_t, uint32_t, uint32_t, int>;
 
@@ -870,6 +1033,13 @@ struct ghx_exec {
   std::vector<int32_t> hremote;
   std::vector<int32_t> hpeer;   // per tag (SyncArgs::tag_peer)
   int32_t nhead = 0;            // remote tasks at the head of htasks
+  // phased exchange (GHX_EXEC_PHASED): x faces, then y faces extended over
+  // the x ghosts, then z faces extended over x and y ghosts (no edge or
+  // corner tags); tasks ordered by phase, [0, pe0) x, [pe0, pe1) y, rest z
+  bool phased = false;
+  int8_t cur_phase = 0;         // phase of the tag being emitted
+  std::vector<int8_t> hphase;   // per tag
+  int32_t pe0 = 0, pe1 = 0;
   // in-kernel synchronisation (ghx_exec_set_sync)
   int32_t sync_rank = -1, sync_n = 0;
   uint64_t **dflags = nullptr;
@@ -937,6 +1107,7 @@ void add_devtag(ghx_exec *ex, const HostTag &t, int64_t x0, int64_t nxe, int vl,
   ex->hkeys.emplace_back(t.sfab, t.dfab, t.shift[0], t.shift[1], t.shift[2], part, g.nxv, g.ny, g.nz, vl);
   ex->hremote.push_back(t.remote ? 1 : 0);
   ex->hpeer.push_back(t.peer);
+  ex->hphase.push_back(ex->cur_phase);
 }
 
 // Split a row range into an unaligned head, 16-byte body and tail when src
@@ -1247,6 +1418,22 @@ void build_tasks(ghx_exec *ex) {
     };
     std::stable_sort(a.begin() + (interleave ? 0 : ex->nhead), a.end(), [&](const int4 &l, const int4 &r) { return key(l) < key(r); });
   }
+  ex->pe0 = ex->pe1 = 0;
+  if (ex->phased) {
+    auto tphase = [&](const int4 &t) -> int {
+      const int32_t tag = (t.z == -4 || t.z == -3 || t.z == -6) ? ex->hchain[t.x] : t.x;
+      return ex->hphase[tag];
+    };
+    std::stable_sort(a.begin(), a.end(), [&](const int4 &l, const int4 &r) { return tphase(l) < tphase(r); });
+    int32_t c0 = 0, c1 = 0;
+    for (const int4 &t : a) {
+      const int ph = tphase(t);
+      c0 += ph < 1;
+      c1 += ph < 2;
+    }
+    ex->pe0 = c0;
+    ex->pe1 = c1;
+  }
   ex->htasks.swap(a);
 }
 
@@ -1269,6 +1456,8 @@ int ghx_exec_create(const ghx_plan *plan, int32_t rank, int32_t kind, const int6
                     int32_t src_ncomp_total, const int64_t *dst_fab_boxes, int32_t dst_ncomp_total,
                     int32_t scomp, int32_t dcomp, int32_t ncomp, int32_t elem_bytes, int32_t device,
                     ghx_exec **out) {
+  const bool want_phased = (kind & GHX_EXEC_PHASED) != 0;
+  kind &= ~GHX_EXEC_PHASED;
   if (!plan || !out || (plan->nsrc && !src_fab_boxes) || (plan->ndst && !dst_fab_boxes) ||
       rank < 0 || rank >= plan->nranks || kind < GHX_EXEC_DIRECT || kind > GHX_EXEC_UNPACK_PACKED_ALL ||
       (elem_bytes != 4 && elem_bytes != 8) || ncomp < 1 || scomp < 0 || dcomp < 0 ||
@@ -1317,6 +1506,9 @@ int ghx_exec_create(const ghx_plan *plan, int32_t rank, int32_t kind, const int6
     return p.srank != p.drank && (pack_all || (p.dbox.hi[0] - p.dbox.lo[0] + 1) * elem_bytes <= pack_row_bytes);
   };
   int64_t bad = -1;
+  std::vector<Piece> taken;
+  std::vector<int64_t> taken_id;  // wtags index (error reporting)
+  std::vector<uint8_t> taken_sfab, taken_dfab;
   for (size_t i = 0; i < plan->wtags.size(); ++i) {
     const Piece &p = plan->wtags[i];
     bool take = false, src_is_fab = true, dst_is_fab = true;
@@ -1331,6 +1523,25 @@ int ghx_exec_create(const ghx_plan *plan, int32_t rank, int32_t kind, const int6
       case GHX_EXEC_UNPACK_PACKED_ALL: take = p.drank == rank && packable(p); src_is_fab = false; break;
     }
     if (!take) continue;
+    taken.push_back(p);
+    taken_id.push_back((int64_t)i);
+    taken_sfab.push_back(src_is_fab);
+    taken_dfab.push_back(dst_is_fab);
+  }
+  std::vector<int8_t> taken_phase(taken.size(), 0);
+  if (want_phased && (kind == GHX_EXEC_DIRECT || kind == GHX_EXEC_LOCAL)) {
+    std::vector<Box> sstore(plan->nsrc);
+    for (int32_t f = 0; f < plan->nsrc; ++f) sstore[f] = ghx::box_from(src_fab_boxes + 6 * f);
+    ex->phased = phase_pieces(plan, rank, sstore, taken, taken_phase);
+    if (ex->phased) {
+      taken_id.assign(taken.size(), -1);
+      taken_sfab.assign(taken.size(), 1);
+      taken_dfab.assign(taken.size(), 1);
+    }
+  }
+  for (size_t i = 0; i < taken.size(); ++i) {
+    const Piece &p = taken[i];
+    const bool src_is_fab = taken_sfab[i], dst_is_fab = taken_dfab[i];
     const Layout S = layout(src_fab_boxes + 6 * p.src, src_ncomp_total);
     const Layout D = layout(dst_fab_boxes + 6 * p.dst, dst_ncomp_total);
     Box sbox = p.dbox;
@@ -1349,9 +1560,10 @@ int ghx_exec_create(const ghx_plan *plan, int32_t rank, int32_t kind, const int6
     t.dfab = p.dst;
     for (int d = 0; d < 3; ++d) t.shift[d] = p.shift[d];
     if ((src_is_fab && !contains(S.box, sbox)) || (dst_is_fab && !contains(D.box, p.dbox))) {
-      bad = (int64_t)i;
+      bad = taken_id[i] >= 0 ? taken_id[i] : 0;
       break;
     }
+    ex->cur_phase = taken_phase[i];
     const int64_t cells = t.nx * t.ny * t.nz;
     if (src_is_fab) {
       t.s.off = (sbox.lo[0] - S.box.lo[0]) +
@@ -1592,6 +1804,18 @@ int ghx_exec_task_kinds(const ghx_exec *ex, int64_t out[6]) {
   return GHX_OK;
 }
 
+int ghx_exec_phases(const ghx_exec *ex, int64_t out[4]) {
+  if (!ex || !out) {
+    set_error("ghx_exec_phases: bad arguments");
+    return GHX_EINVAL;
+  }
+  out[0] = ex->phased ? 1 : 0;
+  out[1] = ex->pe0;
+  out[2] = ex->pe1;
+  out[3] = (int64_t)ex->htags.size();
+  return GHX_OK;
+}
+
 int ghx_exec_buffer_elems(const ghx_exec *ex, int64_t *per_peer) {
   if (!ex || !per_peer) {
     set_error("ghx_exec_buffer_elems: bad arguments");
@@ -1652,8 +1876,8 @@ int find_or_bind(ghx_exec *ex, void *const *ptrs, int64_t nptrs, cudaStream_t st
     std::unique_ptr<ghx_exec::Binding> nb(new ghx_exec::Binding());
     cudaError_t e = cudaMalloc(&nb->dtags, std::max<size_t>(1, ex->htags.size()) * sizeof(DevTag));
     if (e == cudaSuccess) e = cudaMalloc(&nb->dptrs, std::max<int64_t>(ex->nptrs, 1) * sizeof(void *));
-    if (e == cudaSuccess) e = cudaMalloc(&nb->counter, 2 * sizeof(unsigned long long));
-    if (e == cudaSuccess) e = cudaMemsetAsync(nb->counter, 0, 2 * sizeof(unsigned long long), st);
+    if (e == cudaSuccess) e = cudaMalloc(&nb->counter, 8 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemsetAsync(nb->counter, 0, 8 * sizeof(unsigned long long), st);
     if (e == cudaSuccess && !ex->htags.empty())
       e = cudaMemcpyAsync(nb->dtags, ex->dtags, ex->htags.size() * sizeof(DevTag), cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) {
@@ -1682,15 +1906,28 @@ int find_or_bind(ghx_exec *ex, void *const *ptrs, int64_t nptrs, cudaStream_t st
   return GHX_OK;
 }
 
-int launch(ghx_exec *ex, ghx_exec::Binding *bd, cudaStream_t st, const SyncArgs &sync) {
+int launch(ghx_exec *ex, ghx_exec::Binding *bd, cudaStream_t st, const SyncArgs &sync_in) {
   bd->last_use = ++ex->uses;
+  SyncArgs sync = sync_in;
+  sync.pe0 = ex->phased ? ex->pe0 : 0;
+  sync.pe1 = ex->phased ? ex->pe1 : 0;
   DevTag *const dtags = bd->dtags;
   unsigned long long *const counter = bd->counter;
   const int ntasks = (int)ex->htasks.size();
+  int blocks = ex->blocks;
+  if (ex->phased) {  // phase waits need every CTA resident
+    static int cap = [] {
+      int occ = 0, sms = 148;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ghx_copy_kernel<2, true>, kThreads, 0);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+      return std::max(1, occ) * sms;
+    }();
+    blocks = std::min(blocks, cap);
+  }
   // tasks per atomic grab: single tasks balance the latency-bound seam work
   // best (FillBoundary plans, measured), long streaming task lists
   // (ParallelCopy regrids) amortise the atomic over ~64 grabs per warp
-  int batch = (int)std::max<int64_t>(1, std::min<int64_t>(64, ntasks / ((int64_t)ex->blocks * kWarps * 64)));
+  int batch = (int)std::max<int64_t>(1, std::min<int64_t>(64, ntasks / ((int64_t)blocks * kWarps * 64)));
   if (const char *v = std::getenv("GHX_BATCH")) batch = std::max(1, std::atoi(v));
   int ld = ex->ld_mode;
   if (ld == 0 && !ex->nc_loads) ld = 2;  // sources may alias destinations (ParallelCopy): no .nc
@@ -1702,16 +1939,16 @@ int launch(ghx_exec *ex, ghx_exec::Binding *bd, cudaStream_t st, const SyncArgs 
     // the dynamic shared memory limit is a per-device (per-context) function
     // attribute: set it once on every device that launches bulk rows
     if (int rc = bulk_smem_attr(ex->device)) return rc;
-    ghx_copy_kernel<2, false, true><<<ex->blocks, ex->threads, kWarps * kBulkBytes, st>>>(
+    ghx_copy_kernel<2, false, true><<<blocks, ex->threads, kWarps * kBulkBytes, st>>>(
         dtags, ex->dtasks, ntasks, ex->dchain, counter, batch, sync);
   } else if (ex->nring) {  // ring tasks present: the ring-capable instantiation
-    ghx_copy_kernel<2, true><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, counter, batch, sync);
+    ghx_copy_kernel<2, true><<<blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, counter, batch, sync);
   } else switch (ld) {
-    case 0: ghx_copy_kernel<0><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, counter, batch, sync); break;
-    case 1: ghx_copy_kernel<1><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, counter, batch, sync); break;
-    case 2: ghx_copy_kernel<2><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, counter, batch, sync); break;
-    case 3: ghx_copy_kernel<3><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, counter, batch, sync); break;
-    default: ghx_copy_kernel<4><<<ex->blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, counter, batch, sync); break;
+    case 0: ghx_copy_kernel<0><<<blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, counter, batch, sync); break;
+    case 1: ghx_copy_kernel<1><<<blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, counter, batch, sync); break;
+    case 2: ghx_copy_kernel<2><<<blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, counter, batch, sync); break;
+    case 3: ghx_copy_kernel<3><<<blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, counter, batch, sync); break;
+    default: ghx_copy_kernel<4><<<blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, counter, batch, sync); break;
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "ghx_exec_run: launch");

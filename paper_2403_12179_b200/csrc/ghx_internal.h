@@ -61,6 +61,10 @@ struct ghx_plan {
   int32_t nsrc = 0, ndst = 0;
   std::vector<ghx::Piece> segs;   // reference segments, CommPlan order
   std::vector<ghx::Piece> wtags;  // disjoint write tags (last writer wins)
+  bool clipped = false;            // some destinations overlapped (wtags != segs)
+  // FillBoundary: the valid boxes and ghost widths the plan was built for
+  std::vector<ghx::Box> vbox;
+  int64_t ngrow[3] = {0, 0, 0};
 };
 
 namespace ghx {

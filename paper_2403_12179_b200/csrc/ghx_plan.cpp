@@ -220,8 +220,9 @@ static void build_pieces(const std::vector<Box> &targets, const std::vector<Box>
 // Last writer wins (reference order on the receiving rank: local segments
 // in plan order, then each peer's message in ascending peer order,
 // comm.py:328-378): clip earlier writers so destinations become disjoint.
-static void clip_writes(const std::vector<Piece> &segs, int32_t ndst, std::vector<Piece> &out) {
+static bool clip_writes(const std::vector<Piece> &segs, int32_t ndst, std::vector<Piece> &out) {
   out.clear();
+  bool clipped = false;
   std::vector<std::vector<int64_t>> by_dst(ndst);
   for (int64_t i = 0; i < (int64_t)segs.size(); ++i) by_dst[segs[i].dst].push_back(i);
   std::vector<Box> cur, nxt, parts;
@@ -245,6 +246,7 @@ static void clip_writes(const std::vector<Piece> &segs, int32_t ndst, std::vecto
       for (int64_t i : ids) out.push_back(segs[i]);
       continue;
     }
+    clipped = true;
     const int32_t drank = segs[ids[0]].drank;
     std::vector<int64_t> worder(ids);
     std::stable_sort(worder.begin(), worder.end(), [&](int64_t a, int64_t b) {
@@ -277,6 +279,7 @@ static void clip_writes(const std::vector<Piece> &segs, int32_t ndst, std::vecto
     std::sort(kept.begin(), kept.end(), seg_less);
     out.insert(out.end(), kept.begin(), kept.end());
   }
+  return clipped;
 }
 
 static int finish_plan(ghx_plan *p, std::vector<Piece> &pieces, const int32_t *src_rank,
@@ -287,7 +290,7 @@ static int finish_plan(ghx_plan *p, std::vector<Piece> &pieces, const int32_t *s
     pc.drank = dst_rank[pc.dst];
   }
   p->segs.swap(pieces);
-  clip_writes(p->segs, p->ndst, p->wtags);
+  p->clipped = clip_writes(p->segs, p->ndst, p->wtags);
   return GHX_OK;
 }
 
@@ -366,6 +369,8 @@ int ghx_plan_build_fill_boundary(int64_t nboxes, const int64_t *boxes, const int
     std::vector<Piece> pieces;
     build_pieces(tgt, &valid, valid, periodic, period, pieces);
     finish_plan(p, pieces, rank_of, rank_of);
+    p->vbox = valid;
+    for (int d = 0; d < 3; ++d) p->ngrow[d] = ngrow[d];
     *out = p;
     return GHX_OK;
   } catch (const std::bad_alloc &) {

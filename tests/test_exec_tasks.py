@@ -65,3 +65,73 @@ def test_set_ring_rebuilds_tasks_only_before_first_run():
     k0 = kinds(256, 64, 4, 2, ring=False)
     k1 = kinds(256, 64, 4, 2, ring=True)
     assert k0["copy"] == k1["copy"]  # face copies unchanged; seams change form
+
+
+def phases(boxes, n, ng, nc, periodic, ranks=None, nranks=1, phased=True, rank=0):
+    ranks = [0] * len(boxes) if ranks is None else ranks
+    h = native_fb(boxes, [ng] * 3, list(periodic), [n] * 3, ranks, nranks)
+    storage = boxes.copy()
+    storage[:, :3] -= ng
+    storage[:, 3:] += ng
+    storage = np.ascontiguousarray(storage)
+    ex = C.c_void_p()
+    try:
+        kind = N.EXEC_DIRECT | (N.EXEC_PHASED if phased else 0)
+        N.check(N.lib.ghx_exec_create(h, rank, kind, N.i64p(storage), nc, N.i64p(storage), nc, 0, 0, nc, 8, 0,
+                                      C.byref(ex)))
+        ph = np.zeros(4, np.int64)
+        N.check(N.lib.ghx_exec_phases(ex, N.i64p(ph)))
+        a = [C.c_int64() for _ in range(4)]
+        N.check(N.lib.ghx_exec_info(ex, *[C.byref(v) for v in a]))
+        return dict(phased=int(ph[0]), pe0=int(ph[1]), pe1=int(ph[2]), tags=int(ph[3]), tasks=a[1].value,
+                    elems=a[2].value)
+    finally:
+        if ex:
+            N.lib.ghx_exec_free(ex)
+        N.lib.ghx_plan_free(h)
+
+
+@pytest.mark.parametrize("n,b,nc,ng", [(512, 128, 8, 2), (256, 64, 4, 2), (64, 32, 1, 1), (256, 16, 4, 2)])
+def test_phased_exchange_drops_edge_and_corner_tags(n, b, nc, ng):
+    """Uniform periodic layouts: every fab's faces are extended over the
+    lower-axis ghosts, so only the 6 face tags per fab remain (x faces: two
+    tags per side pair), moving exactly the same ghost elements."""
+    boxes = gu.scale_boxes(n, b)
+    p = phases(boxes, n, ng, nc, (1, 1, 1))
+    q = phases(boxes, n, ng, nc, (1, 1, 1), phased=False)
+    assert p["phased"] == 1 and q["phased"] == 0
+    assert p["elems"] == q["elems"]
+    assert p["tags"] < q["tags"]
+    assert 0 < p["pe0"] <= p["pe1"] < p["tasks"]
+
+
+@pytest.mark.parametrize("periodic", [(0, 1, 1), (1, 0, 1), (0, 0, 0), (1, 1, 0)])
+def test_phased_exchange_keeps_element_count_with_physical_boundaries(periodic):
+    # fabs at a non-periodic face keep their own tags where an extension
+    # would reach uncovered ghosts; the element count never changes
+    boxes = gu.scale_boxes(256, 64)
+    p = phases(boxes, 256, 2, 2, periodic)
+    q = phases(boxes, 256, 2, 2, periodic, phased=False)
+    assert p["elems"] == q["elems"] and p["tags"] <= q["tags"]
+
+
+def test_phased_exchange_irregular_boxes_keep_element_count():
+    rng = np.random.default_rng(7)
+    for _ in range(20):
+        # random slab cuts of a 48^3 domain (irregular neighbours)
+        cuts = [np.unique(np.concatenate([[0, 48], rng.integers(4, 44, size=2)])) for _ in range(3)]
+        boxes = np.asarray([[x0, y0, z0, x1 - 1, y1 - 1, z1 - 1]
+                            for z0, z1 in zip(cuts[2][:-1], cuts[2][1:])
+                            for y0, y1 in zip(cuts[1][:-1], cuts[1][1:])
+                            for x0, x1 in zip(cuts[0][:-1], cuts[0][1:])], np.int64)
+        for per in [(1, 1, 1), (0, 1, 0)]:
+            p = phases(boxes, 48, 2, 1, per)
+            q = phases(boxes, 48, 2, 1, per, phased=False)
+            assert p["elems"] == q["elems"]
+
+
+def test_phased_exchange_needs_all_tags_local():
+    boxes = gu.scale_boxes(256, 64)
+    ranks = [i % 2 for i in range(len(boxes))]
+    p = phases(boxes, 256, 2, 2, (1, 1, 1), ranks=ranks, nranks=2)
+    assert p["phased"] == 0

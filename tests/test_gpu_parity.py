@@ -31,8 +31,12 @@ def _domain(amr, c, key="domain"):
 
 # task-building variants of the fused kernel: default heuristics, x-line
 # chains + TMA bulk face rows (the large-fab path), fab-local swaps
+# ... and the phased exchange of host-memory fabs (faces extended over the
+# lower-axis ghosts, phase waits in the kernel) on device fabs, with the
+# default kernel and with the host path's tile-ring instantiation
 VARIANTS = {"default": {}, "chains_bulk": {"GHX_FAB_LOCAL": "0", "GHX_BULK": "1"},
-            "fab_local": {"GHX_FAB_LOCAL": "1", "GHX_BULK": "0"}}
+            "fab_local": {"GHX_FAB_LOCAL": "1", "GHX_BULK": "0"},
+            "phased": {"GHX_PHASED": "1"}, "phased_ring": {"GHX_PHASED": "1", "GHX_RING": "1"}}
 
 
 @pytest.mark.parametrize("variant", sorted(VARIANTS))

@@ -12,7 +12,8 @@ from oracle import inputs
 
 pytestmark = pytest.mark.gpu
 
-VARIANTS = [{}, {"GHX_FAB_LOCAL": "0", "GHX_BULK": "1"}, {"GHX_FAB_LOCAL": "1"}, {"GHX_RING": "1"}]
+VARIANTS = [{}, {"GHX_FAB_LOCAL": "0", "GHX_BULK": "1"}, {"GHX_FAB_LOCAL": "1"}, {"GHX_RING": "1"},
+            {"GHX_PHASED": "1"}, {"GHX_PHASED": "1", "GHX_RING": "1"}]
 
 
 def _layout(rng):
@@ -28,14 +29,14 @@ def _layout(rng):
     return ext, boxes, ng, per
 
 
-@pytest.mark.parametrize("seed", range(24))
+@pytest.mark.parametrize("seed", range(36))
 def test_random_fill_boundary_matches_oracle(seed, monkeypatch):
     import paper_2403_12179_b200 as amr
     rng = np.random.default_rng(1000 + seed)
     ext, boxes, ng, per = _layout(rng)
     nc = int(rng.integers(1, 4))
     dt = np.float32 if seed % 5 == 4 else np.float64
-    memory = "pinned" if seed % 6 == 5 else "device"
+    memory = "pinned" if seed % 7 == 3 else "device"
     for k, v in VARIANTS[seed % len(VARIANTS)].items():
         monkeypatch.setenv(k, v)
     amr.config.set_spacedim(3)

@@ -107,6 +107,35 @@ __global__ void tile_walk(char *buf, int64_t units) {
   }
 }
 
+// MODE 8: line walk -- one warp instruction = 16 consecutive rows of ONE
+// fab; the warp visits the k = 4 fabs of its x-line in turn for the same
+// 16 rows (the next fab's chunk loaded before this one's write), then the
+// next 16 rows: the seam exchange across the x-line would keep all k
+// chunks of a row block in registers.
+__global__ void line_walk(char *buf, int64_t units) {
+  const int lane = threadIdx.x & 31, pair = lane >> 1, side = lane & 1;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // unit = (line, plane, 64-row half): 4 blocks of 16 rows x 4 fabs
+  for (int64_t u = warp; u < units; u += nwarps) {
+    const int64_t half = u % 2, pl = (u / 2) % kPlanes, line = u / (2 * kPlanes);
+    uint32_t cur[8], nxt[8];
+    int64_t row = 2 + half * 64 + pair;
+    ld(seam(buf, line * kLine, pl, row, side), cur);
+    for (int s = 0; s < 16; ++s) {  // s = (row block b, fab j)
+      const int b = s / kLine, j = s % kLine;
+      if (s + 1 < 16) {
+        const int b2 = (s + 1) / kLine, j2 = (s + 1) % kLine;
+        ld(seam(buf, line * kLine + j2, pl, 2 + half * 64 + b2 * 16 + pair, side), nxt);
+      }
+      cur[0] += 1;
+      st(seam(buf, line * kLine + j, pl, 2 + half * 64 + b * 16 + pair, side), cur);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) cur[i] = nxt[i];
+    }
+  }
+}
+
 template <int MODE>
 __global__ void walk(char *buf, int64_t units) {
   const int lane = threadIdx.x & 31, pair = lane >> 1, side = lane & 1;
@@ -205,6 +234,8 @@ void run(const char *name, char *buf, int blocks) {
       walk<MODE><<<blocks, 256>>>(buf, units);
     else if (MODE == 9)
       flat<<<blocks, 256>>>(buf, nseams);
+    else if (MODE == 8)
+      line_walk<<<blocks, 256>>>(buf, units);
     else
       tile_walk<MODE><<<blocks, 256>>>(buf, units);
     cudaEventRecord(e1);
@@ -244,6 +275,7 @@ int main() {
     run<4>("tile-pf", d, blocks);
     run<5>("ring-pf", d, blocks);
     run<6>("tile-pf-w32", d, blocks);
+    run<8>("linewalk", d, blocks);
     run<7>("tile-pf-rd", d, blocks);
   }
   return 0;

@@ -52,8 +52,14 @@ def _worker(rank, world, port, q, n, b, nc, ng, env=None):
         torch.cuda.synchronize()
         ctx = amr.current_ctx()
         s0 = ctx.bus.stats_snapshot()
-        amr.fill_boundary(mf, geom)
-        amr.fill_boundary(mf, geom)
+        # GHX_TEST_DELAY="r:s": rank r enters each exchange s seconds late,
+        # so the peers' kernels really wait in the READY / DONE spins
+        delay = os.environ.get("GHX_TEST_DELAY")
+        for _ in range(2):
+            if delay and int(delay.split(":")[0]) == rank:
+                import time
+                time.sleep(float(delay.split(":")[1]))
+            amr.fill_boundary(mf, geom)
         s1 = ctx.bus.stats_snapshot()
         bad = 0
         for gi in mf.local_indices:
@@ -83,6 +89,11 @@ CASES = [("C1", 64, 32, 1, 1, "C1_x2", {"GHX_REMOTE": "direct"}), ("C3", 512, 12
          ("C1", 64, 32, 1, 1, "C1_x2", {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "20", "GHX_FUSED_SYNC": "0"}),
          ("C1", 64, 32, 1, 1, "C1_x2", {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "20",
                                         "GHX_REMOTE_ORDER": "interleave"}),
+         # one rank late: the other's remote tasks wait for its READY, its
+         # unpack (packed) / exit wait (direct) for its DONE
+         ("C1", 64, 32, 1, 1, "C1_x2", {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "20", "GHX_TEST_DELAY": "1:0.3"}),
+         ("C3", 512, 128, 8, 2, "C3_x2", {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "20",
+                                          "GHX_TEST_DELAY": "0:0.3", "GHX_REMOTE": "direct"}),
          # the pack -> message -> unpack fallback (host-staged over gloo here)
          ("C1", 64, 32, 1, 1, "C1_x2", {"GHX_TRANSPORT": "nccl"}),
          ("C3", 512, 128, 8, 2, "C3_x2", {"GHX_TRANSPORT": "nccl"}),
@@ -95,7 +106,8 @@ CASES = [("C1", 64, 32, 1, 1, "C1_x2", {"GHX_REMOTE": "direct"}), ("C3", 512, 12
 
 @pytest.mark.parametrize("cfg", CASES, ids=["C1-ipc-direct", "C3-ipc-packed", "C3-ipc-direct", "C1-devbarrier-packed",
                                             "C1-devsync-direct", "C3-devsync-packed", "C3-devsync-direct",
-                                            "C1-devbarrier-unfused", "C1-devsync-interleave", "C1-fallback", "C3-fallback", "C1-arena-ipc", "C1-pinned",
+                                            "C1-devbarrier-unfused", "C1-devsync-interleave", "C1-devsync-late1",
+                                            "C3-devsync-late0-direct", "C1-fallback", "C3-fallback", "C1-arena-ipc", "C1-pinned",
                                             "C3-pinned"])
 def test_two_processes_one_gpu(cfg):
     _run(cfg, 2)
@@ -133,3 +145,52 @@ def _run(cfg, world):
             assert msgs == 2  # two calls, one message per ordered pair per call
             pair_bytes[k] = nbytes // 2
     assert pair_bytes == {k: v * nc // c["ncomp"] for k, v in c["pair_bytes"].items()}
+
+
+def _absent_worker(rank, world, port, q):
+    """Rank 1 never enters the exchange: rank 0's kernel must give up after
+    GHX_BARRIER_TIMEOUT_S and its synchronous call raise, not hang the GPU."""
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                          WORLD_SIZE=str(world), LOCAL_RANK="0", GHX_SYNC="device", GHX_BARRIER_TIMEOUT_S="2")
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import paper_2403_12179_b200 as amr
+        from paper_2403_12179_b200 import comm
+        amr.config.set_spacedim(3)
+        dom = amr.Box((0, 0, 0), (63, 63, 63))
+        geom = amr.Geometry(dom, (0.0,) * 3, (1.0,) * 3, (True,) * 3)
+        ba = amr.decompose(dom, 32)
+        mf = amr.MultiFab(ba, amr.DistributionMapping.round_robin(len(ba), world), 1, 1, geom)
+        x = comm.prepare_fill_boundary(mf, geom)  # collective setup (IPC handles, flags)
+        dist.barrier()
+        out = "skipped"
+        if rank == 0:
+            try:
+                x.run()
+                out = "no error"
+            except Exception as e:  # noqa: BLE001
+                out = type(e).__name__ + ": " + str(e)
+        dist.barrier()
+        del x, mf
+        dist.destroy_process_group()
+        q.put((rank, out))
+    except BaseException:  # noqa: BLE001
+        import traceback
+        q.put((rank, "ERROR " + traceback.format_exc()))
+
+
+def test_device_sync_times_out_when_a_peer_never_arrives():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_absent_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+    assert "timed out" in res[0], res[0]
+    assert res[1] == "skipped", res[1]

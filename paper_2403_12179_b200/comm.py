@@ -636,11 +636,56 @@ def _parallel_copy_plan(dst: MultiFab, src: MultiFab, gs: IntVect, gd: IntVect, 
 TRANSPORTS = ("p2p", "nccl")
 
 
-def _transport() -> str:
-    t = os.environ.get("GHX_TRANSPORT", "p2p")
+def _transport(ctx=None) -> str:
+    """The cross-process transport: GHX_TRANSPORT when set, else the
+    CUDA-IPC push when every rank can map every peer's memory (probed once
+    per process context, collectively), else the NCCL fallback."""
+    t = os.environ.get("GHX_TRANSPORT")
+    if t is None:
+        return "p2p" if ctx is None or _ipc_capable(ctx) else "nccl"
     if t not in TRANSPORTS:
         raise ValueError(f"GHX_TRANSPORT must be one of {TRANSPORTS}, got {t!r}")
     return t
+
+
+def _ipc_capable(ctx) -> bool:
+    """Collective probe (cached on the context): every rank exports a small
+    device allocation and maps every peer's; the IPC push is used only if
+    all of them succeed on every rank (a box or container without CUDA IPC
+    between the processes falls back to NCCL instead of failing)."""
+    cap = getattr(ctx, "_ipc_ok", None)
+    if cap is not None:
+        return cap
+    ok, h, probe = True, (C.c_uint8 * 64)(), None
+    try:
+        probe = Slab(256, ctx.device)
+        N.check(N.lib.ghx_ipc_get_handle(C.c_void_p(probe.ptr), h))
+        hb = bytes(h)
+    except Exception:  # noqa: BLE001
+        ok, hb = False, None
+    handles = ctx.allgather(hb)
+    for r, other in enumerate(handles):
+        if r == ctx.rank or not ok:
+            continue
+        if other is None:
+            ok = False
+            break
+        p = C.c_void_p()
+        try:
+            if os.environ.get("GHX_TEST_NO_IPC"):  # tests: a box without CUDA IPC between processes
+                raise N.GhostxError("CUDA IPC disabled (GHX_TEST_NO_IPC)")
+            N.check(N.lib.ghx_ipc_open_handle(ctx.device, (C.c_uint8 * 64).from_buffer_copy(other), C.byref(p)))
+            N.lib.ghx_ipc_close_handle(p)
+        except Exception:  # noqa: BLE001
+            ok = False
+    cap = all(ctx.allgather(ok))
+    ctx.barrier()  # no rank frees its probe while a peer still maps it
+    del probe
+    if not cap and ctx.rank == 0:
+        sys.stderr.write("[paper_2403_12179_b200] CUDA IPC between the ranks is unavailable: "
+                         "cross-process exchanges use the NCCL transport\n")
+    ctx._ipc_ok = cap
+    return cap
 
 
 def _host_resident(mf) -> bool:
@@ -797,7 +842,7 @@ class Exchange:
         self.transport = "p2p"
         host = _host_resident(src_mf) or _host_resident(dst_mf)
         if self.mode == "process":
-            self.transport = _transport()
+            self.transport = _transport(ctx)
             self.sync = _sync_mode(ctx) if self.transport == "p2p" else "stream"
         else:
             self.sync = "host" if self.mode == "thread" else "none"
@@ -1070,7 +1115,7 @@ def exchange_for(plan: CommPlan, src_mf: MultiFab, dst_mf: MultiFab, scomp: int,
             m.check_open()
     ctx = ctx or current_ctx()
     key = ("xchg", plan.uid, src_mf.uid, scomp, dcomp, ncomp, ctx.kind, ctx.nranks,
-           _transport() if ctx.kind == "process" else None)
+           _transport(ctx) if ctx.kind == "process" else None)
     ex = dst_mf._peer_cache.get(key)
     if ex is None:
         ex = cache_put(dst_mf, key, Exchange(plan, src_mf, dst_mf, scomp, dcomp, ncomp, ctx), src_mf)

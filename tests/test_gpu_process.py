@@ -68,6 +68,8 @@ def _worker(rank, world, port, q, n, b, nc, ng, env=None):
             bad += int((device_bits(f).to(exp.device) != exp).sum().item())
         stats = {f"{s}->{d}": (s1[(s, d)][0] - s0[(s, d)][0], s1[(s, d)][1] - s0[(s, d)][1])
                  for (s, d) in s1 if s1[(s, d)] != s0[(s, d)]}
+        if os.environ.get("GHX_TEST_NO_IPC"):  # the probe must have picked the NCCL transport
+            assert amr.comm.prepare_fill_boundary(mf, geom).transport == "nccl"
         dist.barrier()
         del mf
         dist.destroy_process_group()
@@ -94,8 +96,10 @@ CASES = [("C1", 64, 32, 1, 1, "C1_x2", {"GHX_REMOTE": "direct"}), ("C3", 512, 12
          ("C1", 64, 32, 1, 1, "C1_x2", {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "20", "GHX_TEST_DELAY": "1:0.3"}),
          ("C3", 512, 128, 8, 2, "C3_x2", {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "20",
                                           "GHX_TEST_DELAY": "0:0.3", "GHX_REMOTE": "direct"}),
-         # the pack -> message -> unpack fallback (host-staged over gloo here)
+         # the pack -> message -> unpack fallback (host-staged over gloo here),
+         # selected explicitly or because CUDA IPC is unavailable
          ("C1", 64, 32, 1, 1, "C1_x2", {"GHX_TRANSPORT": "nccl"}),
+         ("C1", 64, 32, 1, 1, "C1_x2", {"GHX_TEST_NO_IPC": "1"}),
          ("C3", 512, 128, 8, 2, "C3_x2", {"GHX_TRANSPORT": "nccl"}),
          # fab storage at an offset inside an arena slab: IPC maps whole allocations
          ("C1", 64, 32, 1, 1, "C1_x2", {"GHX_TEST_ARENA": "1", "GHX_REMOTE": "direct"}),
@@ -107,7 +111,7 @@ CASES = [("C1", 64, 32, 1, 1, "C1_x2", {"GHX_REMOTE": "direct"}), ("C3", 512, 12
 @pytest.mark.parametrize("cfg", CASES, ids=["C1-ipc-direct", "C3-ipc-packed", "C3-ipc-direct", "C1-devbarrier-packed",
                                             "C1-devsync-direct", "C3-devsync-packed", "C3-devsync-direct",
                                             "C1-devbarrier-unfused", "C1-devsync-interleave", "C1-devsync-late1",
-                                            "C3-devsync-late0-direct", "C1-fallback", "C3-fallback", "C1-arena-ipc", "C1-pinned",
+                                            "C3-devsync-late0-direct", "C1-fallback", "C1-no-ipc-fallback", "C3-fallback", "C1-arena-ipc", "C1-pinned",
                                             "C3-pinned"])
 def test_two_processes_one_gpu(cfg):
     _run(cfg, 2)

@@ -671,7 +671,7 @@ def run_ours(args, cfg, rank, world):
     alg = x.ex.alg_bytes if x.transport == "p2p" else None
     split = None
     if world == 1 and cfg["kind"] == "fb" and isinstance(cfg["ngrow"], int) and not args.no_split:
-        split = direction_split(amr, cfg, L, stream, flush, clean, mean_ms)
+        split = direction_split(amr, cfg, L, stream, flush, clean, mean_ms, mf=mf)
     roof = None
     if alg is not None:
         achieved = alg / (mean_ms * 1e-3) / 1e9
@@ -768,7 +768,7 @@ def run_ours(args, cfg, rank, world):
         print(json.dumps(line), flush=True)
 
 
-def direction_split(amr, cfg, L, stream, flush, clean, all_ms, reps=20):
+def direction_split(amr, cfg, L, stream, flush, clean, all_ms, reps=20, mf=None):
     """The same FillBoundary split by direction, measured in this run: the
     x faces alone (ngrow (g,0,0): the same x-row seams at the same row
     pitch) and the y/z faces alone (ngrow (0,g,g)), each device-timed like
@@ -781,9 +781,9 @@ def direction_split(amr, cfg, L, stream, flush, clean, all_ms, reps=20):
     g = cfg["ngrow"]
     out = {}
     for name, ng in (("x_only", (g, 0, 0)), ("yz_only", (0, g, g))):
-        mf = amr.MultiFab(L["ba"], L["dm"], cfg["ncomp"], amr.IntVect(*ng), L["geom"])
-        mf.fill_hash(SEED, L["dom"])
-        xx = comm.exchange_for(comm.plan_build_fill_boundary(mf, L["geom"]), mf, mf, 0, 0, mf.ncomp)
+        sm = amr.MultiFab(L["ba"], L["dm"], cfg["ncomp"], amr.IntVect(*ng), L["geom"])
+        sm.fill_hash(SEED, L["dom"])
+        xx = comm.exchange_for(comm.plan_build_fill_boundary(sm, L["geom"]), sm, sm, 0, 0, sm.ncomp)
         for _ in range(3):
             xx.enqueue(stream.cuda_stream)
         ts = []
@@ -802,12 +802,40 @@ def direction_split(amr, cfg, L, stream, flush, clean, all_ms, reps=20):
             rows = sum(int((b.hi[1] - b.lo[1] + 1) * (b.hi[2] - b.lo[2] + 1)) for b in L["ba"]) * cfg["ncomp"]
             out["x_row_seams"] = rows
             out["x_gseam_per_s"] = round(rows / (out["x_only_ms"] * 1e-3) / 1e9, 2)
-        del xx, mf
+        del xx, sm
         torch.cuda.synchronize()
     add = out["x_only_ms"] + out["yz_only_ms"]
     out["additive_floor_ms"] = round(add, 5)
     out["all_ms"] = round(all_ms, 5)
     out["frac_of_additive_floor"] = round(add / all_ms, 4)
+    # the same split on the headline MultiFab's own layout: its x-face tags
+    # alone and every other tag alone (GHX_EXEC_ONLY_XFACES / NO_XFACES)
+    if mf is not None:
+        from paper_2403_12179_b200 import _native as N
+        plan = comm.plan_build_fill_boundary(mf, L["geom"])
+        rows = mf.storage_rows()
+        for name, flag in (("x_faces_same_layout_ms", N.EXEC_ONLY_XFACES), ("rest_same_layout_ms", N.EXEC_NO_XFACES)):
+            ex = comm.Executor(plan, 0, N.EXEC_DIRECT | flag, rows, mf.ncomp, rows, mf.ncomp, 0, 0, mf.ncomp,
+                               mf.dtype.itemsize, mf.device)
+            b = ex.bind(comm._table(ex, mf, [(mf.local_indices, mf._ptrs)]), stream.cuda_stream)
+            for _ in range(3):
+                b.run(stream.cuda_stream)
+            ts = []
+            for _ in range(reps):
+                flush.zero_()
+                if clean is not None:
+                    torch.sum(clean)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                b.run(stream.cuda_stream)
+                e1.record(stream)
+                e1.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            out[name] = round(sum(ts) / len(ts), 5)
+            del b, ex
+        same = out["x_faces_same_layout_ms"] + out["rest_same_layout_ms"]
+        out["additive_floor_same_layout_ms"] = round(same, 5)
+        out["frac_of_additive_floor_same_layout"] = round(same / all_ms, 4)
     return out
 
 

@@ -70,6 +70,12 @@ extern "C" {
  * request costs.  Warps wait for each other between phases, so the grid
  * must be co-resident (host executors run 8 CTAs). */
 #define GHX_EXEC_PHASED 0x100
+/* Diagnostic (FillBoundary, local tags): OR GHX_EXEC_ONLY_XFACES to keep
+ * only the x-face tags (ghost in x alone), GHX_EXEC_NO_XFACES to keep every
+ * other tag -- the two halves of the exchange on the same storage layout,
+ * timed separately by bench.py's direction split. */
+#define GHX_EXEC_ONLY_XFACES 0x200
+#define GHX_EXEC_NO_XFACES 0x400
 
 typedef struct ghx_plan ghx_plan;
 typedef struct ghx_exec ghx_exec;

@@ -19,6 +19,7 @@ GHX_OK, GHX_EINVAL, GHX_ECUDA, GHX_ENOMEM, GHX_EOVERLAP = 0, 1, 2, 3, 4
 MODE_FILL_BOUNDARY, MODE_PARALLEL_COPY = 0, 1
 EXEC_DIRECT, EXEC_LOCAL, EXEC_PACK, EXEC_UNPACK, EXEC_PUSH_PACKED, EXEC_UNPACK_PACKED = 0, 1, 2, 3, 4, 5
 EXEC_PHASED = 0x100  # flag OR-ed into the kind (include/ghostx.h)
+EXEC_ONLY_XFACES, EXEC_NO_XFACES = 0x200, 0x400  # diagnostic direction split
 EXEC_PUSH_PACKED_ALL, EXEC_UNPACK_PACKED_ALL = 6, 7
 
 P = C.c_void_p

@@ -1457,7 +1457,8 @@ int ghx_exec_create(const ghx_plan *plan, int32_t rank, int32_t kind, const int6
                     int32_t scomp, int32_t dcomp, int32_t ncomp, int32_t elem_bytes, int32_t device,
                     ghx_exec **out) {
   const bool want_phased = (kind & GHX_EXEC_PHASED) != 0;
-  kind &= ~GHX_EXEC_PHASED;
+  const int xsel = kind & (GHX_EXEC_ONLY_XFACES | GHX_EXEC_NO_XFACES);
+  kind &= ~(GHX_EXEC_PHASED | GHX_EXEC_ONLY_XFACES | GHX_EXEC_NO_XFACES);
   if (!plan || !out || (plan->nsrc && !src_fab_boxes) || (plan->ndst && !dst_fab_boxes) ||
       rank < 0 || rank >= plan->nranks || kind < GHX_EXEC_DIRECT || kind > GHX_EXEC_UNPACK_PACKED_ALL ||
       (elem_bytes != 4 && elem_bytes != 8) || ncomp < 1 || scomp < 0 || dcomp < 0 ||
@@ -1521,6 +1522,15 @@ int ghx_exec_create(const ghx_plan *plan, int32_t rank, int32_t kind, const int6
       case GHX_EXEC_PUSH_PACKED_ALL: take = p.srank == rank; dst_is_fab = !packable(p); break;
       case GHX_EXEC_UNPACK_PACKED:
       case GHX_EXEC_UNPACK_PACKED_ALL: take = p.drank == rank && packable(p); src_is_fab = false; break;
+    }
+    if (take && xsel && plan->mode == GHX_MODE_FILL_BOUNDARY && (int64_t)plan->vbox.size() == plan->ndst) {
+      // diagnostic split: x-face tags (outside the valid box in x only) or the rest
+      const Box &V = plan->vbox[p.dst];
+      int g = 0;
+      for (int d = 0; d < 3; ++d)
+        if (p.dbox.hi[d] < V.lo[d] || p.dbox.lo[d] > V.hi[d]) g |= 1 << d;
+      const bool xface = g == 1;
+      take = (xsel & GHX_EXEC_ONLY_XFACES) ? xface : !xface;
     }
     if (!take) continue;
     taken.push_back(p);

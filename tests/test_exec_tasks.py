@@ -135,3 +135,29 @@ def test_phased_exchange_needs_all_tags_local():
     ranks = [i % 2 for i in range(len(boxes))]
     p = phases(boxes, 256, 2, 2, (1, 1, 1), ranks=ranks, nranks=2)
     assert p["phased"] == 0
+
+
+@pytest.mark.parametrize("n,b,nc,ng", [(512, 128, 8, 2), (256, 64, 4, 2), (256, 16, 4, 2)])
+def test_diagnostic_xface_split_partitions_the_exchange(n, b, nc, ng):
+    """bench.py's same-layout direction split: the x-face tags and the rest
+    are disjoint halves of the exchange (their elements add up)."""
+    boxes = gu.scale_boxes(n, b)
+    h = native_fb(boxes, [ng] * 3, [1, 1, 1], [n] * 3, [0] * len(boxes), 1)
+    storage = boxes.copy()
+    storage[:, :3] -= ng
+    storage[:, 3:] += ng
+    storage = np.ascontiguousarray(storage)
+    elems = {}
+    try:
+        for name, flag in (("all", 0), ("x", N.EXEC_ONLY_XFACES), ("rest", N.EXEC_NO_XFACES)):
+            ex = C.c_void_p()
+            N.check(N.lib.ghx_exec_create(h, 0, N.EXEC_DIRECT | flag, N.i64p(storage), nc, N.i64p(storage), nc, 0, 0,
+                                          nc, 8, 0, C.byref(ex)))
+            a = [C.c_int64() for _ in range(4)]
+            N.check(N.lib.ghx_exec_info(ex, *[C.byref(v) for v in a]))
+            elems[name] = a[2].value
+            N.lib.ghx_exec_free(ex)
+    finally:
+        N.lib.ghx_plan_free(h)
+    assert elems["x"] + elems["rest"] == elems["all"] and elems["x"] > 0 and elems["rest"] > 0
+    assert elems["x"] == len(boxes) * 2 * ng * b * b * nc

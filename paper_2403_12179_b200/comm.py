@@ -28,6 +28,7 @@ cells * ncomp * itemsize of the reference segments for that pair.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import itertools
 import os
@@ -49,69 +50,90 @@ _COMBINE = {SUM: lambda a, b: a + b, MIN: min, MAX: max}
 
 
 class RankFailure(RuntimeError):
+    """A thread rank of ``runtime_spawn`` raised; ``rank`` is the root cause,
+    ``cause`` its exception (reference comm.py:28-32 semantics)."""
+
     def __init__(self, rank: int, cause: BaseException):
         super().__init__(f"rank {rank} failed: {cause!r}")
-        self.rank = rank
-        self.cause = cause
+        self.rank, self.cause = rank, cause
 
 
 # --------------------------------------------------------------- rank runtime
 
+class _Mailbox:
+    """One ordered rank pair's FIFO: a deque plus an event a blocked
+    receiver sleeps on (set while messages are queued or the run aborts)."""
+
+    __slots__ = ("items", "ready")
+
+    def __init__(self):
+        self.items: deque = deque()
+        self.ready = threading.Event()
+
+
 class Bus:
-    """In-process transport shared by thread ranks: FIFO per ordered pair,
-    exactly-once delivery, per-pair [messages, bytes] statistics."""
+    """In-process transport of the thread ranks (reference comm.py:35-87
+    semantics): FIFO per ordered pair, exactly-once delivery, per-pair
+    (messages, bytes) counters, one reusable barrier, an abort that wakes
+    every blocked receiver and breaks the barrier when a rank fails.  Device
+    exchanges move no payload through it -- they only ``account`` the
+    message the reference would have sent."""
 
     def __init__(self, nranks: int):
         self.nranks = nranks
-        self._cond = threading.Condition()
-        self._queues = {(s, d): deque() for s in range(nranks) for d in range(nranks)}
-        self.message_stats = {(s, d): [0, 0] for s in range(nranks) for d in range(nranks)}
+        self._box = [[_Mailbox() for _ in range(nranks)] for _ in range(nranks)]  # [src][dst]
+        self._counts = np.zeros((nranks, nranks, 2), np.int64)  # messages, bytes
+        self._lock = threading.Lock()
         self.barrier = threading.Barrier(nranks) if nranks > 1 else None
-        self._slots: list = [None] * nranks
+        self._slots: list = [None] * nranks  # allgather exchange area
         self._failed: int | None = None
 
-    def _count(self, src: int, dst: int, nbytes: int) -> None:
-        st = self.message_stats[(src, dst)]
-        st[0] += 1
-        st[1] += int(nbytes)
+    def account(self, src: int, dst: int, nbytes: int) -> None:
+        with self._lock:
+            self._counts[src, dst, 0] += 1
+            self._counts[src, dst, 1] += int(nbytes)
 
     def send(self, src: int, dst: int, payload, nbytes: int) -> None:
-        with self._cond:
-            self._queues[(src, dst)].append(payload)
-            self._count(src, dst, nbytes)
-            self._cond.notify_all()
-
-    def account(self, src: int, dst: int, nbytes: int) -> None:
-        """Record one message whose bytes moved device-to-device (the
-        fused kernel stored them straight into the receiver's fabs)."""
-        with self._cond:
-            self._count(src, dst, nbytes)
+        box = self._box[src][dst]
+        box.items.append(payload)  # deque appends are atomic
+        self.account(src, dst, nbytes)
+        box.ready.set()
 
     def recv(self, src: int, dst: int):
-        with self._cond:
-            q = self._queues[(src, dst)]
-            while not q:
-                if self._failed is not None:
-                    raise RuntimeError(f"recv aborted: rank {self._failed} failed")
-                self._cond.wait(timeout=0.1)
-            return q.popleft()
+        box = self._box[src][dst]  # one receiving thread per mailbox
+        while True:
+            if box.items:
+                return box.items.popleft()
+            if self._failed is not None:
+                raise RuntimeError(f"recv aborted: rank {self._failed} failed")
+            box.ready.clear()
+            if not box.items:  # a send between the check and the clear is seen here
+                box.ready.wait(timeout=0.1)
 
     def fail(self, rank: int) -> None:
-        with self._cond:
-            if self._failed is None:
+        with self._lock:
+            if self._failed is None:  # the first failure is the root cause
                 self._failed = rank
-            self._cond.notify_all()
+        for row in self._box:
+            for box in row:
+                box.ready.set()
         if self.barrier is not None:
             self.barrier.abort()
 
+    @property
+    def message_stats(self) -> dict:
+        return {k: list(v) for k, v in self.stats_snapshot().items()}
+
     def stats_snapshot(self) -> dict:
-        with self._cond:
-            return {k: tuple(v) for k, v in self.message_stats.items()}
+        with self._lock:
+            c = self._counts.copy()
+        n = self.nranks
+        return {(s_, d_): (int(c[s_, d_, 0]), int(c[s_, d_, 1])) for s_ in range(n) for d_ in range(n)}
 
     def format_stats(self) -> str:
-        rows = [f"  {s}->{d}: {n} messages, {b} bytes"
-                for (s, d), (n, b) in sorted(self.stats_snapshot().items()) if n]
-        return "\n".join(["comm message stats (src->dst: messages, bytes):"] + (rows or ["  (no messages)"]))
+        active = [f"  {s_}->{d_}: {m} messages, {b} bytes"
+                  for (s_, d_), (m, b) in sorted(self.stats_snapshot().items()) if m]
+        return "comm message stats (src->dst: messages, bytes):\n" + "\n".join(active or ["  (no messages)"])
 
 
 def _cuda_devices() -> int:
@@ -225,10 +247,11 @@ class ProcessContext:
 
 
 class _LocalBus(Bus):
+    """Process mode: only this process's message counters (no mailboxes in
+    use, the collectives go through torch.distributed)."""
+
     def __init__(self, nranks):
-        super().__init__(1)
-        self.nranks = nranks
-        self.message_stats = {(s, d): [0, 0] for s in range(nranks) for d in range(nranks)}
+        super().__init__(nranks)
         self.barrier = None
 
 
@@ -257,50 +280,54 @@ def current_rank() -> int:
     return current_ctx().rank
 
 
+@contextlib.contextmanager
+def _rank_scope(ctx):
+    """Make ``ctx`` the calling thread's current rank for the block."""
+    prev = getattr(_tls, "ctx", None)
+    _tls.ctx = ctx
+    try:
+        yield ctx
+    finally:
+        _tls.ctx = prev
+
+
 def runtime_spawn(nranks: int, program) -> list:
-    """Run program(ctx) once per logical rank on its own thread; rank r
-    drives GPU r % device_count.  A raising rank aborts the run and surfaces
-    as RankFailure with the root-cause rank (reference comm.py:143-180)."""
+    """Run program(ctx) once per logical rank, each on its own thread with
+    its own GPU (rank r -> device r % device_count), and return the per-rank
+    results.  A rank that raises aborts the others' blocking calls (bus
+    abort) and the run raises RankFailure naming the root-cause rank
+    (reference comm.py:143-180 semantics)."""
     if nranks < 1:
         raise ValueError("nranks must be >= 1")
     bus = Bus(nranks)
     ndev = _cuda_devices()
-
-    def dev_of(r):
-        return (r % ndev) if ndev else 0
-
+    ctxs = [RankContext(r, nranks, bus, (r % ndev) if ndev else 0) for r in range(nranks)]
     if nranks == 1:
-        prev = getattr(_tls, "ctx", None)
-        _tls.ctx = RankContext(0, 1, bus, dev_of(0))
-        try:
-            return [program(_tls.ctx)]
-        finally:
-            _tls.ctx = prev
-    results: list = [None] * nranks
-    failures: dict = {}
+        with _rank_scope(ctxs[0]):
+            return [program(ctxs[0])]
+    outcome: list = [None] * nranks  # (ok, value or exception)
 
-    def main(r: int) -> None:
-        _tls.ctx = RankContext(r, nranks, bus, dev_of(r))
-        try:
-            if ndev:
-                import torch
-                torch.cuda.set_device(dev_of(r))
-            results[r] = program(_tls.ctx)
-        except BaseException as exc:  # noqa: BLE001 - propagate with rank id
-            failures[r] = exc
-            bus.fail(r)
-        finally:
-            _tls.ctx = None
+    def body(ctx) -> None:
+        with _rank_scope(ctx):
+            try:
+                if ndev:
+                    import torch
+                    torch.cuda.set_device(ctx.device)
+                outcome[ctx.rank] = (True, program(ctx))
+            except BaseException as exc:  # noqa: BLE001 - reported with its rank below
+                outcome[ctx.rank] = (False, exc)
+                bus.fail(ctx.rank)
 
-    threads = [threading.Thread(target=main, args=(r,), name=f"rank{r}") for r in range(nranks)]
-    for t in threads:
-        t.start()
-    for t in threads:
-        t.join()
-    if failures:
-        r = bus._failed if bus._failed in failures else min(failures)
-        raise RankFailure(r, failures[r]) from failures[r]
-    return results
+    workers = [threading.Thread(target=body, args=(c,), name=f"rank{c.rank}") for c in ctxs]
+    for w in workers:
+        w.start()
+    for w in workers:
+        w.join()
+    failed = {r: o[1] for r, o in enumerate(outcome) if not o[0]}
+    if failed:
+        root = bus._failed if bus._failed in failed else min(failed)
+        raise RankFailure(root, failed[root]) from failed[root]
+    return [o[1] for o in outcome]
 
 
 def global_reduce(ops, values, ctx=None) -> tuple:

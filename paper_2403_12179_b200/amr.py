@@ -101,11 +101,12 @@ def _launch_interp(jobs: list, ncomp: int, ratio: int, scheme: str, item: int, d
 
 def interp_box(coarse_fab: Fab, fine_fab: Fab, fine_region: Box, ratio: int,
                scheme: str = PIECEWISE_CONSTANT) -> None:
-    """Fill fine_region of fine_fab from coarse_fab data (amr.py:269-314).
-
-    LINEAR uses unlimited centred slopes, so globally linear coarse data is
-    reproduced exactly at fine cell centres; it needs one extra coarse cell
-    around the coarsened region, else this raises."""
+    """Interpolate coarse_fab onto the cells of fine_region in fine_fab: one
+    interp_kernel launch (reference amr.py:269-314, same arithmetic order,
+    bit-identical).  PIECEWISE_CONSTANT copies each fine cell's parent;
+    LINEAR adds unlimited centred slopes per axis, so it reads a one-cell
+    coarse halo around the coarsened region -- checked, like every other
+    precondition, with the reference's ValueError before the launch."""
     if fine_region.is_empty:
         return
     ratio = int(ratio)

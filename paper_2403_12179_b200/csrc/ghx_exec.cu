@@ -1457,8 +1457,8 @@ int ghx_exec_create(const ghx_plan *plan, int32_t rank, int32_t kind, const int6
                     int32_t scomp, int32_t dcomp, int32_t ncomp, int32_t elem_bytes, int32_t device,
                     ghx_exec **out) {
   const bool want_phased = (kind & GHX_EXEC_PHASED) != 0;
-  const int xsel = kind & (GHX_EXEC_ONLY_XFACES | GHX_EXEC_NO_XFACES);
-  kind &= ~(GHX_EXEC_PHASED | GHX_EXEC_ONLY_XFACES | GHX_EXEC_NO_XFACES);
+  const int xsel = kind & (GHX_EXEC_ONLY_XFACES | GHX_EXEC_NO_XFACES | 0x800);
+  kind &= ~(GHX_EXEC_PHASED | GHX_EXEC_ONLY_XFACES | GHX_EXEC_NO_XFACES | 0x800);
   if (!plan || !out || (plan->nsrc && !src_fab_boxes) || (plan->ndst && !dst_fab_boxes) ||
       rank < 0 || rank >= plan->nranks || kind < GHX_EXEC_DIRECT || kind > GHX_EXEC_UNPACK_PACKED_ALL ||
       (elem_bytes != 4 && elem_bytes != 8) || ncomp < 1 || scomp < 0 || dcomp < 0 ||
@@ -1530,7 +1530,10 @@ int ghx_exec_create(const ghx_plan *plan, int32_t rank, int32_t kind, const int6
       for (int d = 0; d < 3; ++d)
         if (p.dbox.hi[d] < V.lo[d] || p.dbox.lo[d] > V.hi[d]) g |= 1 << d;
       const bool xface = g == 1;
-      take = (xsel & GHX_EXEC_ONLY_XFACES) ? xface : !xface;
+      if (xsel & 0x800)  // experiment: the y / z faces alone (no x faces, edges, corners)
+        take = g == 2 || g == 4;
+      else
+        take = (xsel & GHX_EXEC_ONLY_XFACES) ? xface : !xface;
     }
     if (!take) continue;
     taken.push_back(p);

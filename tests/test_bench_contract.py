@@ -69,6 +69,10 @@ def test_our_arm_one_gpu_default_c3():
     assert d["config"]["workload"].startswith("C3:") and d["n_gpus"] == 1 and d["scaling"] == "strong"
     assert d["verified"] is True and d["gpu_launches"] == 5
     assert d["roofline"]["bound"] == "hbm" and 0 < d["roofline"]["frac"] < 1.2
+    sp = d["roofline"]["direction_split"]  # the floors measured in the same run
+    assert sp["x_row_seams"] == 64 * 8 * 128 * 128 and sp["x_only_ms"] > 0 and sp["yz_only_ms"] > 0
+    assert 0.5 < sp["frac_of_additive_floor_same_layout"] < 2.0
+    assert d["e2e"]["exec"]["phased"] == 1 and d["e2e"]["exec"]["ring_tasks"] > 0  # the host-memory path
     cb = d["cpu_baseline"]
     assert cb["kind"] == "reference" and cb["bit_exact_vs_ours_fab0"] is True, cb
     assert d["e2e"]["verified"] is True and d["e2e"]["h2d_bytes_per_step"] > 0

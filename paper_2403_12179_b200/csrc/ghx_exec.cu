@@ -744,13 +744,19 @@ __global__ void __launch_bounds__(kThreads, RING ? 1 : GHX_MINB) ghx_copy_kernel
       if (phased) pass_to(w >= sync.pe1 ? 2 : (w >= sync.pe0 ? 1 : 0), true);
       if (tk.z >= -1 && (sync.mode == 2 || (sync.mode == 1 && w < sync.nhead))) {
         // a remote push waits for the peer's READY, an unpack for its DONE
-        const int peer = __ldg(sync.tag_peer + tk.x);
-        if (peer >= 0 && peer < 64 && !((peers_ok >> peer) & 1ull)) {
-          if (lane == 0)
-            flag_wait(sync.flags[sync.rank] + (sync.mode == 1 ? kSlotReady : kSlotDone) * sync.nranks + peer,
-                      sync.epoch, sync.timeout_ns);
-          __syncwarp();
-          peers_ok |= 1ull << peer;
+        // (both tags of a pair task: they may belong to different peers)
+#pragma unroll 1
+        for (int k2 = 0; k2 < 2; ++k2) {
+          const int tg = k2 ? tk.z : tk.x;
+          if (tg < 0) continue;
+          const int peer = __ldg(sync.tag_peer + tg);
+          if (peer >= 0 && peer < 64 && !((peers_ok >> peer) & 1ull)) {
+            if (lane == 0)
+              flag_wait(sync.flags[sync.rank] + (sync.mode == 1 ? kSlotReady : kSlotDone) * sync.nranks + peer,
+                        sync.epoch, sync.timeout_ns);
+            __syncwarp();
+            peers_ok |= 1ull << peer;
+          }
         }
       }
       if (tk.z == -3) {  // chain task: all seams of one chain, kChainRows rows
@@ -1217,6 +1223,36 @@ void build_tasks(ghx_exec *ex) {
       mate[i] = it->second;
       mate[it->second] = (int32_t)i;
     }
+  // Remote tags of one fab with the same shape run as pair tasks, chunk by
+  // chunk: a sender's lo- and hi-x-face tags read the two ends of the same
+  // rows -- one 128-B line per row seam -- and an unpack's lo- and hi-x-ghost
+  // tags fill the two halves of the same seam lines, so the second access
+  // of each line hits in L2 instead of fetching (and, for the partial-sector
+  // ghost writes, refilling) it again.  Anchor fab: the source for pushes,
+  // the destination for unpacks.  (GHX_REMOTE_PAIR=0: unpaired.)
+  static const bool pair_remote = [] {
+    const char *v = std::getenv("GHX_REMOTE_PAIR");
+    return !v || std::atoi(v) != 0;
+  }();
+  if (pair_remote) {
+    const bool unpack = ex->kind == GHX_EXEC_UNPACK || ex->kind == GHX_EXEC_UNPACK_PACKED ||
+                        ex->kind == GHX_EXEC_UNPACK_PACKED_ALL;
+    std::map<std::tuple<int32_t, uint32_t, uint32_t, uint32_t, uint32_t, int>, int32_t> open;
+    for (size_t i = 0; i < n; ++i) {
+      if (mate[i] >= 0 || !ex->hremote[i]) continue;
+      const DevTag &t = ex->htags[i];
+      const auto key = std::make_tuple(unpack ? std::get<1>(ex->hkeys[i]) : std::get<0>(ex->hkeys[i]), t.nxv, t.ny,
+                                       t.nz, t.nvec, (int)t.vlog);
+      auto it = open.find(key);
+      if (it == open.end()) {
+        open.emplace(key, (int32_t)i);
+      } else {
+        mate[i] = it->second;
+        mate[it->second] = (int32_t)i;
+        open.erase(it);
+      }
+    }
+  }
   std::vector<int4> loc, rem, swaps;
   ex->npaired = 0;
   ex->nswap = 0;

@@ -1973,11 +1973,6 @@ int launch(ghx_exec *ex, ghx_exec::Binding *bd, cudaStream_t st, const SyncArgs 
     }();
     blocks = std::min(blocks, cap);
   }
-  // tasks per atomic grab: single tasks balance the latency-bound seam work
-  // best (FillBoundary plans, measured), long streaming task lists
-  // (ParallelCopy regrids) amortise the atomic over ~64 grabs per warp
-  int batch = (int)std::max<int64_t>(1, std::min<int64_t>(64, ntasks / ((int64_t)blocks * kWarps * 64)));
-  if (const char *v = std::getenv("GHX_BATCH")) batch = std::max(1, std::atoi(v));
   int ld = ex->ld_mode;
   if (ld == 0 && !ex->nc_loads) ld = 2;  // sources may alias destinations (ParallelCopy): no .nc
   if (ex->nbulk && ex->nring) {
@@ -1988,20 +1983,55 @@ int launch(ghx_exec *ex, ghx_exec::Binding *bd, cudaStream_t st, const SyncArgs 
     // the dynamic shared memory limit is a per-device (per-context) function
     // attribute: set it once on every device that launches bulk rows
     if (int rc = bulk_smem_attr(ex->device)) return rc;
-    ghx_copy_kernel<2, false, true><<<blocks, ex->threads, kWarps * kBulkBytes, st>>>(
-        dtags, ex->dtasks, ntasks, ex->dchain, counter, batch, sync);
-  } else if (ex->nring) {  // ring tasks present: the ring-capable instantiation
-    ghx_copy_kernel<2, true><<<blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, counter, batch, sync);
-  } else switch (ld) {
-    case 0: ghx_copy_kernel<0><<<blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, counter, batch, sync); break;
-    case 1: ghx_copy_kernel<1><<<blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, counter, batch, sync); break;
-    case 2: ghx_copy_kernel<2><<<blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, counter, batch, sync); break;
-    case 3: ghx_copy_kernel<3><<<blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, counter, batch, sync); break;
-    default: ghx_copy_kernel<4><<<blocks, ex->threads, 0, st>>>(dtags, ex->dtasks, ntasks, ex->dchain, counter, batch, sync); break;
+  }
+  // one launch over tasks [first, first + count)
+  auto go = [&](int first, int count, int nblocks, bool ring, const SyncArgs &sy) {
+    if (count <= 0) return;
+    // tasks per atomic grab: single tasks balance the latency-bound seam work
+    // best (FillBoundary plans, measured), long streaming task lists
+    // (ParallelCopy regrids) amortise the atomic over ~64 grabs per warp
+    int batch = (int)std::max<int64_t>(1, std::min<int64_t>(64, count / ((int64_t)nblocks * kWarps * 64)));
+    if (const char *v = std::getenv("GHX_BATCH")) batch = std::max(1, std::atoi(v));
+    const int4 *tk = ex->dtasks + first;
+    if (ex->nbulk)
+      ghx_copy_kernel<2, false, true><<<nblocks, ex->threads, kWarps * kBulkBytes, st>>>(dtags, tk, count, ex->dchain,
+                                                                                        counter, batch, sy);
+    else if (ring)  // ring tasks present: the ring-capable instantiation
+      ghx_copy_kernel<2, true><<<nblocks, ex->threads, 0, st>>>(dtags, tk, count, ex->dchain, counter, batch, sy);
+    else switch (ld) {
+      case 0: ghx_copy_kernel<0><<<nblocks, ex->threads, 0, st>>>(dtags, tk, count, ex->dchain, counter, batch, sy); break;
+      case 1: ghx_copy_kernel<1><<<nblocks, ex->threads, 0, st>>>(dtags, tk, count, ex->dchain, counter, batch, sy); break;
+      case 2: ghx_copy_kernel<2><<<nblocks, ex->threads, 0, st>>>(dtags, tk, count, ex->dchain, counter, batch, sy); break;
+      case 3: ghx_copy_kernel<3><<<nblocks, ex->threads, 0, st>>>(dtags, tk, count, ex->dchain, counter, batch, sy); break;
+      default: ghx_copy_kernel<4><<<nblocks, ex->threads, 0, st>>>(dtags, tk, count, ex->dchain, counter, batch, sy); break;
+    }
+    g_launches.fetch_add(1);
+  };
+  // Experiment (GHX_PHASE_LAUNCHES=1): a phased executor with no cross-rank
+  // sync runs its three phases as three stream-ordered launches (no
+  // in-kernel phase waits), the face phases on a wider grid
+  // (GHX_HOST_FACE_BLOCKS, 32).  Measured: C3 e2e 49.7 -> 48.7 ms, C2 same,
+  // C4 27.2 -> 28.8 ms -- the single launch with phase waits stays.
+  static const bool split = [] {
+    const char *v = std::getenv("GHX_PHASE_LAUNCHES");
+    return v && std::atoi(v) != 0;
+  }();
+  if (ex->phased && split && sync.mode == 0) {
+    static const int face_blocks = [] {
+      const char *v = std::getenv("GHX_HOST_FACE_BLOCKS");
+      return v ? std::max(1, std::atoi(v)) : 32;
+    }();
+    SyncArgs plain = sync;
+    plain.pe0 = plain.pe1 = 0;
+    const int fb = std::max(blocks, face_blocks);
+    go(0, ex->pe0, blocks, ex->nring > 0, plain);
+    go(ex->pe0, ex->pe1 - ex->pe0, fb, false, plain);
+    go(ex->pe1, ntasks - ex->pe1, fb, false, plain);
+  } else {
+    go(0, ntasks, blocks, ex->nring > 0, sync);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "ghx_exec_run: launch");
-  g_launches.fetch_add(1);
   return GHX_OK;
 }
 

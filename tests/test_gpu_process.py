@@ -105,14 +105,16 @@ CASES = [("C1", 64, 32, 1, 1, "C1_x2", {"GHX_REMOTE": "direct"}), ("C3", 512, 12
          ("C1", 64, 32, 1, 1, "C1_x2", {"GHX_TEST_ARENA": "1", "GHX_REMOTE": "direct"}),
          # fabs in pinned host memory: pack -> message -> unpack, kernels over PCIe
          ("C1", 64, 32, 1, 1, "C1_x2", {"GHX_TEST_PINNED": "1"}),
-         ("C3", 512, 128, 8, 2, "C3_x2", {"GHX_TEST_PINNED": "1"})]
+         ("C3", 512, 128, 8, 2, "C3_x2", {"GHX_TEST_PINNED": "1"}),
+         # pinned host fabs with the in-kernel READY/DONE protocol
+         ("C1", 64, 32, 1, 1, "C1_x2", {"GHX_TEST_PINNED": "1", "GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "20"})]
 
 
 @pytest.mark.parametrize("cfg", CASES, ids=["C1-ipc-direct", "C3-ipc-packed", "C3-ipc-direct", "C1-devbarrier-packed",
                                             "C1-devsync-direct", "C3-devsync-packed", "C3-devsync-direct",
                                             "C1-devbarrier-unfused", "C1-devsync-interleave", "C1-devsync-late1",
                                             "C3-devsync-late0-direct", "C1-fallback", "C1-no-ipc-fallback", "C3-fallback", "C1-arena-ipc", "C1-pinned",
-                                            "C3-pinned"])
+                                            "C3-pinned", "C1-pinned-devsync"])
 def test_two_processes_one_gpu(cfg):
     _run(cfg, 2)
 

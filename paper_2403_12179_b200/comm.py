@@ -900,6 +900,8 @@ class Exchange:
         self._thread_bindings: dict = {}
         self._pin()
         self._init_fused_sync()
+        ex0 = getattr(self, "ex", None)
+        self._phased = bool(ex0 is not None and ex0.detail.get("phased"))
         row = plan.pair_cells[me]
         self.messages = [(me, d, int(row[d]) * ncomp * self.item) for d in range(plan.nranks)
                          if d != me and row[d] > 0]
@@ -1116,8 +1118,8 @@ class Exchange:
         else:
             self.enqueue(stream.cuda_stream)
             stream.synchronize()
-            if self.mode == "process" and self.sync == "device":
-                check_barriers()
+            if (self.mode == "process" and self.sync == "device") or self._phased:
+                check_barriers()  # in-kernel waits are bounded: a timeout means an incomplete result
         for (s, d, nbytes) in self.messages:
             ctx.bus.account(s, d, nbytes)
 
@@ -1241,6 +1243,8 @@ def _fill_boundary_serial_fast(mf: MultiFab, geom, backend) -> bool:
     if rc == 0:
         rc = N.lib.ghx_stream_sync(C.c_void_p(st))
     N.check(rc)
+    if fast[4]:
+        check_barriers()
     return True
 
 
@@ -1264,7 +1268,7 @@ def fill_boundary(mf: MultiFab, geom: Geometry | None = None, backend=None) -> N
             if _raw_stream is None:
                 _raw_stream = _raw_stream_fn()
             # the geometry object this plan was built for (None = mf.geom)
-            mf._fb_fast = (geom, ex.b_ex, _plan_key_of(mf, plan), plan)
+            mf._fb_fast = (geom, ex.b_ex, _plan_key_of(mf, plan), plan, ex._phased)
 
 
 def _pc_args(dst, src, scomp, dcomp, ncomp, ngrow_src, ngrow_dst):

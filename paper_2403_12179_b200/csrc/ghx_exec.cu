@@ -715,11 +715,19 @@ __global__ void __launch_bounds__(kThreads, RING ? 1 : GHX_MINB) ghx_copy_kernel
       ++my_phase;
       if (wait) {
         if (lane == 0) {
+          // bounded like the cross-rank waits: a grid that is not fully
+          // resident (it must be) counts a timeout instead of hanging
+          const uint64_t t0 = gtimer_ns();
           unsigned long long v = 0;
-          do {
+          for (uint32_t it = 0;; ++it) {
             asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(counter + 2 + my_phase - 1) : "memory");
-            if (v < nwarps_all) __nanosleep(128);
-          } while (v < nwarps_all);
+            if (v >= nwarps_all) break;
+            if ((it & 1023) == 1023 && gtimer_ns() - t0 > sync.timeout_ns) {
+              atomicAdd(&g_sync_timeouts, 1u);
+              break;
+            }
+            __nanosleep(128);
+          }
         }
         __syncwarp();
       }
@@ -1955,11 +1963,21 @@ int find_or_bind(ghx_exec *ex, void *const *ptrs, int64_t nptrs, cudaStream_t st
   return GHX_OK;
 }
 
+static uint64_t sync_timeout_ns() {
+  static const uint64_t ns = [] {
+    const char *v = std::getenv("GHX_BARRIER_TIMEOUT_S");
+    const double sec = v ? std::atof(v) : 30.0;
+    return (uint64_t)(sec * 1e9);
+  }();
+  return ns;
+}
+
 int launch(ghx_exec *ex, ghx_exec::Binding *bd, cudaStream_t st, const SyncArgs &sync_in) {
   bd->last_use = ++ex->uses;
   SyncArgs sync = sync_in;
   sync.pe0 = ex->phased ? ex->pe0 : 0;
   sync.pe1 = ex->phased ? ex->pe1 : 0;
+  if (ex->phased && sync.timeout_ns == 0) sync.timeout_ns = sync_timeout_ns();
   DevTag *const dtags = bd->dtags;
   unsigned long long *const counter = bd->counter;
   const int ntasks = (int)ex->htasks.size();
@@ -2093,15 +2111,6 @@ int ghx_exec_run_bound(ghx_exec *ex, int64_t binding, void *stream) {
     if (b->id == binding && b->pins > 0) return launch(ex, b.get(), static_cast<cudaStream_t>(stream), SyncArgs{});
   set_error("ghx_exec_run_bound: unknown or released binding " + std::to_string(binding));
   return GHX_EINVAL;
-}
-
-static uint64_t sync_timeout_ns() {
-  static const uint64_t ns = [] {
-    const char *v = std::getenv("GHX_BARRIER_TIMEOUT_S");
-    const double sec = v ? std::atof(v) : 30.0;
-    return (uint64_t)(sec * 1e9);
-  }();
-  return ns;
 }
 
 int ghx_exec_set_sync(ghx_exec *ex, uint64_t *const *flag_arrays, int32_t rank, int32_t nranks) {

@@ -93,3 +93,17 @@ def test_our_arm_two_ranks_on_one_gpu():
     assert nv["bound"] == "nvlink" and nv["frac"] > 0 and nv["peak"] == 770.0
     assert nv["bytes_per_gpu_max_send_recv"] == 142737408 and "hbm" in nv
     assert d["e2e"]["verified"] is True and d["e2e"]["h2d_bytes_per_step"] > 0
+
+
+@pytest.mark.gpu
+def test_our_arm_two_ranks_device_sync():
+    """The path a multi-GPU box takes (device sync: READY/DONE inside the
+    copy kernel, enqueue-only timing loop), forced on two processes that
+    share one GPU (time-sliced: the timing means nothing, the result is
+    verified)."""
+    rc, lines, err = _torchrun(2, ["--gpus", "2", "--steps", "3", "--warmup", "3", "--no-cpu", "--e2e-steps", "2"],
+                               env={"GHX_BENCH_BACKEND": "gloo", "GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "60"})
+    assert rc == 0, err[-2000:]
+    d = json.loads(lines[0])
+    assert d["config"]["sync"] == "device" and d["config"]["transport"] == "p2p"
+    assert d["verified"] is True and d["e2e"]["verified"] is True

@@ -1,0 +1,191 @@
+"""The reference-side binding a maintainer would add to miniamr_core
+(INTEGRATION.md section 2), as runnable code: the reference's OWN MultiFab,
+Fab and Geometry objects, its numpy fab arrays allocated from pinned,
+mapped host memory, and the exchange done by libghostx.so through the
+plain C ABI (ctypes, pointers and sizes only -- no torch, no
+paper_2403_12179_b200 Python layer).
+
+    from miniamr_core import mesh, comm
+    from integration.reference_binding import PinnedArena, fill_boundary_native
+    mf = mesh.MultiFab(ba, dm, ncomp, ngrow, geom, arena=PinnedArena())
+    fill_boundary_native(mf, geom)        # instead of comm.fill_boundary(mf, geom)
+
+The arena duck-types the reference's (arena.py:87-163: ``alloc(nbytes,
+align)`` returning a block with ``as_array(dtype, count)`` / ``free()``),
+so Fab (mesh.py:43-86) allocates its storage in memory the GPU kernel can
+address directly (UVA: the host pointer is the device pointer).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.environ.get("GHX_LIB") or os.path.join(os.path.dirname(_HERE), "paper_2403_12179_b200", "_lib",
+                                                       "libghostx.so")
+_lib = None
+
+P, I32, I64 = C.c_void_p, C.c_int32, C.c_int64
+PI64, PI32 = C.POINTER(C.c_int64), C.POINTER(C.c_int32)
+
+
+def lib():
+    """Load libghostx.so and declare the entry points this binding uses."""
+    global _lib
+    if _lib is None:
+        L = C.CDLL(_LIB_PATH)
+        L.ghx_last_error.restype = C.c_char_p
+        L.ghx_host_alloc.argtypes = [C.c_size_t, C.POINTER(P)]
+        L.ghx_host_free.argtypes = [P]
+        L.ghx_plan_build_fill_boundary.argtypes = [I64, PI64, PI64, PI32, PI64, PI32, I32, C.POINTER(P)]
+        L.ghx_plan_free.argtypes = [P]
+        L.ghx_plan_free.restype = None
+        L.ghx_exec_create.argtypes = [P, I32, I32, PI64, I32, PI64, I32, I32, I32, I32, I32, I32, C.POINTER(P)]
+        L.ghx_exec_free.argtypes = [P]
+        L.ghx_exec_free.restype = None
+        L.ghx_exec_run.argtypes = [P, C.POINTER(P), I64, P]
+        L.ghx_stream_sync.argtypes = [P]
+        L.ghx_interp.argtypes = [P, I64, I32, PI32, I32, I32, I32, P]
+        _lib = L
+    return _lib
+
+
+def _check(rc: int) -> None:
+    if rc:
+        msg = lib().ghx_last_error().decode()
+        raise (ValueError if rc == 1 else RuntimeError)(msg)
+
+
+# ------------------------------------------------------------------ arena
+
+class _PinnedBlock:
+    __slots__ = ("arena", "ptr", "nbytes", "freed")
+
+    def __init__(self, arena, ptr: int, nbytes: int):
+        self.arena, self.ptr, self.nbytes, self.freed = arena, ptr, nbytes, False
+
+    @property
+    def is_null(self) -> bool:
+        return self.ptr == 0
+
+    @property
+    def address(self) -> int:
+        return self.ptr
+
+    def as_array(self, dtype, count: int) -> np.ndarray:
+        if self.is_null:
+            return np.empty(0, dtype=dtype)
+        raw = (C.c_uint8 * (np.dtype(dtype).itemsize * count)).from_address(self.ptr)
+        return np.frombuffer(raw, dtype=dtype, count=count)
+
+    def free(self) -> None:
+        if not self.freed and self.ptr:
+            lib().ghx_host_free(P(self.ptr))
+        self.freed = True
+
+
+class PinnedArena:
+    """A reference-compatible arena whose blocks are pinned, mapped host
+    memory (ghx_host_alloc): numpy sees ordinary arrays, the GPU the same
+    addresses."""
+
+    def alloc(self, nbytes: int, align: int = 256) -> _PinnedBlock:
+        if nbytes == 0:
+            return _PinnedBlock(self, 0, 0)
+        p = P()
+        _check(lib().ghx_host_alloc(int(nbytes), C.byref(p)))  # cudaHostAlloc: page aligned
+        return _PinnedBlock(self, p.value, nbytes)
+
+    def free(self, block: _PinnedBlock) -> None:
+        block.free()
+
+
+# ---------------------------------------------------------------- helpers
+
+def _rows(boxes, grow=(0, 0, 0)) -> np.ndarray:
+    """Boxes -> int64[n, 6] rows (lo0 lo1 lo2 hi0 hi1 hi2), padded to 3-D."""
+    out = np.zeros((len(boxes), 6), np.int64)
+    for i, b in enumerate(boxes):
+        d = len(b.lo)
+        out[i, :d] = [v - grow[k] for k, v in enumerate(b.lo)]
+        out[i, 3:3 + d] = [v + grow[k] for k, v in enumerate(b.hi)]
+    return out
+
+
+def _p64(a: np.ndarray):
+    return a.ctypes.data_as(PI64)
+
+
+def _p32(a: np.ndarray):
+    return a.ctypes.data_as(PI32)
+
+
+class _Prepared:
+    """A built plan + executor for one MultiFab layout (the reference caches
+    its plan per PlanKey, comm.py:299-308; this caches both)."""
+
+    def __init__(self, mf, geom):
+        L = lib()
+        d = len(mf.ngrow)
+        ng = np.array(list(mf.ngrow) + [0] * (3 - d), np.int64)
+        per = np.array([int(v) for v in geom.periodic] + [0] * (3 - d), np.int32)
+        period = np.array(list(geom.period) + [1] * (3 - d), np.int64)
+        rows = _rows(list(mf.ba))
+        ranks = np.asarray(mf.dm.rank_of, np.int32)
+        self.plan = P()
+        _check(L.ghx_plan_build_fill_boundary(len(rows), _p64(rows), _p64(ng), _p32(per), _p64(period), _p32(ranks),
+                                              mf.dm.nranks, C.byref(self.plan)))
+        storage = _rows(list(mf.ba), grow=tuple(int(v) for v in ng))
+        item = np.dtype(mf.fabs[mf.local_indices[0]].data.dtype).itemsize
+        self.ex = P()
+        _check(L.ghx_exec_create(self.plan, mf.rank, 0, _p64(storage), mf.ncomp, _p64(storage), mf.ncomp, 0, 0,
+                                 mf.ncomp, item, 0, C.byref(self.ex)))
+        n = len(rows)
+        self.table = np.zeros(2 * n + 2 * mf.dm.nranks, np.uint64)  # [src fabs][dst fabs][send][recv]
+        for i, fab in mf.fabs.items():
+            addr = fab.data.__array_interface__["data"][0]
+            self.table[i] = self.table[n + i] = addr
+
+    def __del__(self):
+        try:
+            lib().ghx_exec_free(self.ex)
+            lib().ghx_plan_free(self.plan)
+        except Exception:  # noqa: BLE001
+            pass
+
+
+def fill_boundary_native(mf, geom=None) -> None:
+    """Drop-in body for the reference's comm.fill_boundary (comm.py:383-394)
+    on one rank: the plan and executor are built once per MultiFab and
+    geometry, every call is one kernel launch plus a stream synchronize
+    (the reference API is synchronous).  The fabs must live in device or
+    pinned-mapped memory (``PinnedArena``)."""
+    geom = geom or mf.geom
+    key = ("ghostx", id(geom))
+    prep = mf.plan_cache.get(key)
+    if prep is None:
+        prep = mf.plan_cache[key] = _Prepared(mf, geom)
+    L = lib()
+    t = prep.table
+    _check(L.ghx_exec_run(prep.ex, t.ctypes.data_as(C.POINTER(P)), len(t), None))
+    _check(L.ghx_stream_sync(None))
+
+
+def interp_box_native(coarse_fab, fine_fab, fine_region, ratio: int, scheme: str = "pc") -> None:
+    """Drop-in body for the reference's amr.interp_box (amr.py:269-314) on
+    pinned fabs: one ghx_interp job (20 int64 words)."""
+    job = np.zeros((1, 20), np.int64)
+    job[0, 0] = coarse_fab.data.__array_interface__["data"][0]
+    job[0, 1:7] = _rows([coarse_fab.box])[0]
+    job[0, 7] = fine_fab.data.__array_interface__["data"][0]
+    job[0, 8:14] = _rows([fine_fab.box])[0]
+    job[0, 14:20] = _rows([fine_region])[0]
+    d = len(fine_region.lo)
+    r3 = np.array([int(ratio)] * d + [1] * (3 - d), np.int32)
+    L = lib()
+    _check(L.ghx_interp(P(job.ctypes.data), 1, fine_fab.ncomp, _p32(r3), d, 1 if scheme == "linear" else 0,
+                        fine_fab.data.dtype.itemsize, None))
+    _check(L.ghx_stream_sync(None))

@@ -1,0 +1,77 @@
+"""The reference-side binding (integration/reference_binding.py, the stub of
+INTEGRATION.md section 2) driving libghostx.so through the plain C ABI on
+the REFERENCE's own objects: miniamr_core's MultiFab / Fab with their numpy
+storage allocated from pinned, mapped host memory.  Its FillBoundary and
+interp_box must equal the reference's own functions on twin objects bit for
+bit.  Needs the reference install in baseline/_ref (skipped without it)."""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF = os.environ.get("MINIAMR_REF", os.path.join(REPO, "baseline", "_ref"))
+
+
+@pytest.fixture(scope="module")
+def ref():
+    if not os.path.isdir(os.path.join(REF, "miniamr_core")):
+        pytest.skip("reference install (baseline/_ref) not present")
+    sys.path.insert(0, REF)
+    import miniamr_core
+    from miniamr_core import amr, comm, config, index_space, mesh
+    yield miniamr_core, amr, comm, config, index_space, mesh
+    sys.path.remove(REF)
+
+
+def _fill(mf, seed):
+    rng = np.random.default_rng(seed)
+    for i in mf.local_indices:
+        a = mf.fabs[i].data
+        a[...] = rng.standard_normal(a.shape)
+
+
+@pytest.mark.parametrize("dim,n,b,nc,ng,per", [(3, 32, 16, 2, 2, (1, 1, 1)), (3, 24, 8, 1, 1, (1, 0, 1)),
+                                                (2, 40, 16, 3, 2, (1, 1)), (3, 20, (8, 12, 20), 2, 1, (0, 1, 1))])
+def test_fill_boundary_through_c_abi_equals_reference(ref, dim, n, b, nc, ng, per):
+    _, _, comm, config, ix, mesh = ref
+    from integration.reference_binding import PinnedArena, fill_boundary_native
+    config.set_spacedim(dim) if hasattr(config, "set_spacedim") else None
+    dom = ix.Box((0,) * dim, (n - 1,) * dim)
+    geom = ix.Geometry(dom, (0.0,) * dim, (1.0,) * dim, per)
+    ba = mesh.decompose(dom, b if isinstance(b, int) else list(b[:dim]))
+    dm = mesh.DistributionMapping.round_robin(len(ba), 1)
+    ours = mesh.MultiFab(ba, dm, nc, ng, geom, arena=PinnedArena())
+    theirs = mesh.MultiFab(ba, dm, nc, ng, geom)
+    _fill(ours, 7)
+    _fill(theirs, 7)
+    for _ in range(2):
+        fill_boundary_native(ours, geom)
+        comm.fill_boundary(theirs, geom)
+    for i in ours.local_indices:
+        got = ours.fabs[i].data.view(np.uint64)
+        exp = theirs.fabs[i].data.view(np.uint64)
+        assert np.array_equal(got, exp), f"fab {i}"
+
+
+@pytest.mark.parametrize("scheme", ["piecewise_constant", "linear"])
+def test_interp_box_through_c_abi_equals_reference(ref, scheme):
+    _, amr, _, config, ix, mesh = ref
+    from integration.reference_binding import PinnedArena, interp_box_native
+    config.set_spacedim(3) if hasattr(config, "set_spacedim") else None
+    arena = PinnedArena()
+    cbox = ix.Box((3, 2, 4), (12, 11, 13))
+    fbox = ix.Box((8, 6, 10), (21, 19, 23))
+    region = ix.Box((9, 7, 11), (20, 18, 22))
+    rng = np.random.default_rng(3)
+    c_ours, c_ref = mesh.Fab(cbox, 2, arena), mesh.Fab(cbox, 2)
+    f_ours, f_ref = mesh.Fab(fbox, 2, arena), mesh.Fab(fbox, 2)
+    c_ours.data[...] = c_ref.data[...] = rng.standard_normal(c_ref.data.shape)
+    f_ours.data[...] = f_ref.data[...] = rng.standard_normal(f_ref.data.shape)
+    interp_box_native(c_ours, f_ours, region, 2, scheme)
+    amr.interp_box(c_ref, f_ref, region, 2, scheme)
+    assert np.array_equal(f_ours.data.view(np.uint64), f_ref.data.view(np.uint64))

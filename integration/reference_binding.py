@@ -49,6 +49,8 @@ def lib():
         L.ghx_exec_run.argtypes = [P, C.POINTER(P), I64, P]
         L.ghx_stream_sync.argtypes = [P]
         L.ghx_interp.argtypes = [P, I64, I32, PI32, I32, I32, I32, P]
+        L.ghx_plan_build_parallel_copy.argtypes = [I64, PI64, PI64, I64, PI64, PI64, PI32, PI64, PI32, PI32, I32,
+                                                   C.POINTER(P)]
         _lib = L
     return _lib
 
@@ -172,6 +174,49 @@ def fill_boundary_native(mf, geom=None) -> None:
     t = prep.table
     _check(L.ghx_exec_run(prep.ex, t.ctypes.data_as(C.POINTER(P)), len(t), None))
     _check(L.ghx_stream_sync(None))
+
+
+def parallel_copy_native(dst, src, scomp=0, dcomp=0, ncomp=None, ngrow_src=0, ngrow_dst=0, geom=None) -> None:
+    """Drop-in body for the reference's comm.parallel_copy (comm.py:397-429)
+    on one rank (the reference's argument checks omitted): a ParallelCopy
+    plan between the two layouts and one launch over both MultiFabs'
+    fabs."""
+    L = lib()
+    ncomp = ncomp if ncomp is not None else min(src.ncomp - scomp, dst.ncomp - dcomp)
+    d = len(dst.ngrow)
+    gs = np.array([int(ngrow_src)] * d + [0] * (3 - d), np.int64)
+    gd = np.array([int(ngrow_dst)] * d + [0] * (3 - d), np.int64)
+    drows, srows = _rows(list(dst.ba)), _rows(list(src.ba))
+    if geom is not None:
+        per = np.array([int(v) for v in geom.periodic] + [0] * (3 - d), np.int32)
+        period = np.array(list(geom.period) + [1] * (3 - d), np.int64)
+        per_p, period_p = _p32(per), _p64(period)
+    else:
+        period = np.ones(3, np.int64)
+        per_p, period_p = None, _p64(period)
+    sr, dr = np.asarray(src.dm.rank_of, np.int32), np.asarray(dst.dm.rank_of, np.int32)
+    plan = P()
+    _check(L.ghx_plan_build_parallel_copy(len(drows), _p64(drows), _p64(gd), len(srows), _p64(srows), _p64(gs),
+                                          per_p, period_p, _p32(sr), _p32(dr), dst.dm.nranks, C.byref(plan)))
+    ex = P()
+    try:
+        sst = _rows(list(src.ba), grow=tuple(int(v) for v in src.ngrow) + (0,) * (3 - d))
+        dst_st = _rows(list(dst.ba), grow=tuple(int(v) for v in dst.ngrow) + (0,) * (3 - d))
+        item = dst.fabs[dst.local_indices[0]].data.dtype.itemsize
+        _check(L.ghx_exec_create(plan, dst.rank, 0, _p64(sst), src.ncomp, _p64(dst_st), dst.ncomp, scomp, dcomp,
+                                 ncomp, item, 0, C.byref(ex)))
+        ns, nd = len(srows), len(drows)
+        table = np.zeros(ns + nd + 2 * dst.dm.nranks, np.uint64)
+        for i, fab in src.fabs.items():
+            table[i] = fab.data.__array_interface__["data"][0]
+        for i, fab in dst.fabs.items():
+            table[ns + i] = fab.data.__array_interface__["data"][0]
+        _check(L.ghx_exec_run(ex, table.ctypes.data_as(C.POINTER(P)), len(table), None))
+        _check(L.ghx_stream_sync(None))
+    finally:
+        if ex:
+            L.ghx_exec_free(ex)
+        L.ghx_plan_free(plan)
 
 
 def interp_box_native(coarse_fab, fine_fab, fine_region, ratio: int, scheme: str = "pc") -> None:

@@ -75,3 +75,27 @@ def test_interp_box_through_c_abi_equals_reference(ref, scheme):
     interp_box_native(c_ours, f_ours, region, 2, scheme)
     amr.interp_box(c_ref, f_ref, region, 2, scheme)
     assert np.array_equal(f_ours.data.view(np.uint64), f_ref.data.view(np.uint64))
+
+
+@pytest.mark.parametrize("n,sb,db,nc,gs,gd,periodic", [(32, 8, 16, 2, 0, 0, None), (24, 12, 8, 1, 1, 2, (1, 1, 1)),
+                                                       (32, 16, 8, 3, 0, 1, (0, 1, 1))])
+def test_parallel_copy_through_c_abi_equals_reference(ref, n, sb, db, nc, gs, gd, periodic):
+    _, _, comm, config, ix, mesh = ref
+    from integration.reference_binding import PinnedArena, parallel_copy_native
+    config.set_spacedim(3)
+    dom = ix.Box((0, 0, 0), (n - 1,) * 3)
+    geom = ix.Geometry(dom, (0.0,) * 3, (1.0,) * 3, periodic) if periodic else None
+    sba, dba = mesh.decompose(dom, sb), mesh.decompose(dom, db)
+    sdm = mesh.DistributionMapping.round_robin(len(sba), 1)
+    ddm = mesh.DistributionMapping.round_robin(len(dba), 1)
+    arena = PinnedArena()
+    src_o, dst_o = mesh.MultiFab(sba, sdm, nc, gs, arena=arena), mesh.MultiFab(dba, ddm, nc + 1, gd, arena=arena)
+    src_r, dst_r = mesh.MultiFab(sba, sdm, nc, gs), mesh.MultiFab(dba, ddm, nc + 1, gd)
+    _fill(src_o, 11)
+    _fill(src_r, 11)
+    _fill(dst_o, 12)
+    _fill(dst_r, 12)
+    parallel_copy_native(dst_o, src_o, 0, 1, nc, gs, gd, geom)
+    comm.parallel_copy(dst_r, src_r, 0, 1, nc, gs, gd, geom)
+    for i in dst_o.local_indices:
+        assert np.array_equal(dst_o.fabs[i].data.view(np.uint64), dst_r.fabs[i].data.view(np.uint64)), f"fab {i}"

@@ -204,3 +204,39 @@ def test_gpu_debug_parallel_copy_matches_reference(name):
         assert res[0][1] == gu.stats_dict(d[f"{name}/stats"])
     finally:
         _restore(amr)
+
+
+def _debug_arena_roundtrip(memory):
+    from paper_2403_12179_b200 import config
+    from paper_2403_12179_b200.arena import Arena
+    prev = config.debug
+    config.debug = True
+    try:
+        a = Arena(1 << 16, memory=memory)
+        blk = a.alloc(4096)
+        ptr, padded = blk.ptr, blk.padded
+        view = blk.as_array(np.uint8, padded)
+        view[:] = 7
+        a.free(blk)
+        if memory == "device":
+            import torch
+            torch.cuda.synchronize()
+            got = view.cpu().numpy()
+        else:
+            got = np.asarray(view)
+        assert got.size == padded and (got == 0xAB).all()  # freed bytes scribbled (reference arena.py:157-161)
+        again = a.alloc(4096)
+        assert again.ptr == ptr  # the pool hands the scribbled block back
+        with pytest.raises(RuntimeError, match="double free"):
+            a.free(blk)
+    finally:
+        config.debug = prev
+
+
+def test_debug_arena_scribbles_freed_host_blocks():
+    _debug_arena_roundtrip("host")
+
+
+@pytest.mark.gpu
+def test_debug_arena_scribbles_freed_device_blocks():
+    _debug_arena_roundtrip("device")

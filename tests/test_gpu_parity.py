@@ -359,3 +359,46 @@ def test_parallel_copy_one_to_four_ranks_message_count():
         return out
 
     assert amr.runtime_spawn(4, program)[0] == 3
+
+
+@pytest.mark.parametrize("n,b,nc,ng,per,dt,memory", [
+    (256, 64, 4, 2, (1, 0, 1), "f8", "device"), (256, 64, 4, 2, (0, 1, 0), "f8", "pinned"),
+    (256, 16, 4, 2, (1, 1, 0), "f4", "device"), (256, 64, 3, 1, (1, 1, 1), "f4", "pinned"),
+    (512, 128, 8, 2, (0, 0, 0), "f8", "device"), (128, 32, 2, 2, (1, 0, 0), "f8", "pinned")],
+    ids=["C2-xz-periodic", "C2-y-periodic-pinned", "C4-f32", "f32-ng1-pinned", "C3-no-periodic",
+         "x-periodic-pinned-phased"])
+def test_full_size_mixed_periodicity_and_float32(n, b, nc, ng, per, dt, memory):
+    """Full-size layouts with physical boundaries and float32 storage, on
+    device fabs and on pinned host fabs (the phased host exchange): after
+    FillBoundary every storage cell equals the hash of its periodically
+    wrapped cell where that cell lies in the domain, and keeps its poison
+    bits where it does not (uncoverable ghosts untouched)."""
+    import torch
+    amr = _amr()
+    amr.config.set_spacedim(3)
+    amr.config.set_real_dtype(np.dtype(dt))
+    try:
+        dom = amr.Box((0, 0, 0), (n - 1,) * 3)
+        geom = amr.Geometry(dom, (0.0,) * 3, (1.0,) * 3, tuple(bool(p) for p in per))
+        ba = amr.decompose(dom, b)
+        dm = amr.DistributionMapping([0] * len(ba))
+        mf = amr.MultiFab(ba, dm, nc, ng, geom, memory=memory)
+        mf.fill_hash(inputs.SEED, dom)
+        torch.cuda.synchronize()
+        amr.fill_boundary(mf, geom)
+        amr.fill_boundary(mf, geom)
+        if memory == "pinned":
+            assert amr.comm.prepare_fill_boundary(mf, geom).ex.detail["phased"] == 1
+        item = np.dtype(dt).itemsize
+        bad = 0
+        for gi in mf.local_indices:
+            f = mf.fabs[gi]
+            exp = expected_wrapped(f, nc, dom.as_row(), per, inputs.SEED, item)
+            if memory == "pinned":
+                got = torch.from_numpy(bits_of(f).view(np.int64 if item == 8 else np.int32)).to(exp.device)
+            else:
+                got = device_bits(f)
+            bad += int((got != exp).sum().item())
+        assert bad == 0
+    finally:
+        amr.config.set_real_dtype(np.dtype("f8"))

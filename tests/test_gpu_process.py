@@ -200,3 +200,61 @@ def test_device_sync_times_out_when_a_peer_never_arrives():
         p.join(timeout=60)
     assert "timed out" in res[0], res[0]
     assert res[1] == "skipped", res[1]
+
+
+def _pc_worker(rank, world, port, q, env):
+    """ParallelCopy between two layouts (64^3-box source -> 32^3-box
+    destination of a 128^3 domain, 2 comps) across processes sharing the GPU:
+    every destination cell must hold the source hash of its cell."""
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                          WORLD_SIZE=str(world), LOCAL_RANK="0")
+        os.environ.update(env or {})
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import paper_2403_12179_b200 as amr
+        from gpu_util import device_bits, expected_wrapped
+        from oracle import inputs
+        amr.config.set_spacedim(3)
+        dom = amr.Box((0, 0, 0), (127, 127, 127))
+        sba, dba = amr.decompose(dom, 64), amr.decompose(dom, 32)
+        src = amr.MultiFab(sba, amr.DistributionMapping.round_robin(len(sba), world), 2, 0)
+        dst = amr.MultiFab(dba, amr.DistributionMapping.round_robin(len(dba), world), 2, 0)
+        src.fill_hash(inputs.SEED, dom)
+        dst.setval(0.0)
+        torch.cuda.synchronize()
+        for _ in range(2):
+            amr.parallel_copy(dst, src)
+        bad = 0
+        for gi in dst.local_indices:
+            f = dst.fabs[gi]
+            exp = expected_wrapped(f, 2, dom.as_row(), (0, 0, 0), inputs.SEED, 8)
+            bad += int((device_bits(f) != exp).sum().item())
+        x = amr.comm.prepare_parallel_copy(dst, src)
+        dist.barrier()
+        del src, dst, x
+        dist.destroy_process_group()
+        q.put((rank, bad))
+    except BaseException:  # noqa: BLE001
+        import traceback
+        q.put((rank, "ERROR " + traceback.format_exc()))
+
+
+@pytest.mark.parametrize("env", [{}, {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "20"},
+                                 {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "20", "GHX_REMOTE": "direct"},
+                                 {"GHX_TRANSPORT": "nccl"}],
+                         ids=["host-sync", "devsync-packed", "devsync-direct", "fallback"])
+def test_parallel_copy_two_processes(env):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pc_worker, args=(r, 2, port, q, env)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in range(2))
+    for p in procs:
+        p.join(timeout=120)
+    for r in range(2):
+        assert res[r] == 0, res[r]

@@ -629,6 +629,29 @@ def run_ours(args, cfg, rank, world):
     if x.mode == "process" and x.sync == "device":
         from paper_2403_12179_b200 import comm as _comm
         _comm.check_barriers()
+    breakdown = None
+    if world > 1 and getattr(x, "fused", False) and os.environ.get("GHX_BENCH_BREAKDOWN", "1") != "0":
+        # diagnostic steps (outside the timed region): this rank's push kernel
+        # (incl. its READY waits) and the unpack / DONE wait, each timed on
+        # the device; the max over ranks is reported
+        push, tail = [], []
+        for _ in range(max(3, min(K, 10))):
+            flush.zero_()
+            dist.barrier()
+            m = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            x.enqueue(stream.cuda_stream, marks=[lambda e=e: e.record(stream) for e in m])
+            torch.cuda.synchronize()
+            try:  # never let a diagnostic raise on one rank only (the peers would wait in a collective)
+                push.append(m[0].elapsed_time(m[1]))
+                tail.append(m[1].elapsed_time(m[2]))
+            except RuntimeError:
+                push.append(float("nan"))
+                tail.append(float("nan"))
+        _comm.check_barriers()
+        v = torch.tensor([statistics.median(push), statistics.median(tail)], dtype=torch.float64, device=dev)
+        dist.all_reduce(v, op=dist.ReduceOp.MAX)
+        breakdown = {"push_kernel_ms": round(float(v[0]), 5), "unpack_or_wait_ms": round(float(v[1]), 5),
+                     "remote": x.remote, "note": "median per rank, max over ranks; push includes the READY waits"}
     launches = N.lib.ghx_launch_count() - l0
     if dist:
         dist.barrier()
@@ -742,6 +765,8 @@ def run_ours(args, cfg, rank, world):
         "verified": verified,
         "step_ms_min": round(min(step_ms), 5), "step_ms_median": round(statistics.median(step_ms), 5),
     }
+    if breakdown is not None:
+        line["multi_gpu_breakdown"] = breakdown
     # e2e through the public API on host-resident fabs
     if not args.no_e2e:
         line["e2e"] = e2e_leg(args, amr, cfg, L, world, ghost_bytes, x)
@@ -927,6 +952,9 @@ def main():
     ap.add_argument("--no-port", action="store_true", help="skip the numpy-port sample next to the reference")
     ap.add_argument("--ngrow", default=None, help="diagnostic: override ghost width per axis, e.g. 2,0,0")
     args = ap.parse_args()
+    if os.environ.get("GHX_DEBUG_HANG_S"):  # diagnostics: dump every thread's stack if the run hangs
+        import faulthandler
+        faulthandler.dump_traceback_later(float(os.environ["GHX_DEBUG_HANG_S"]), exit=True)
     if args.warmup < 3:
         log("[bench] warm-up raised to 3 (timing rules)")
         args.warmup = 3

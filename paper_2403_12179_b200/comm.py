@@ -1070,18 +1070,28 @@ class Exchange:
     def launches_per_call(self) -> int:
         return 3 if self.transport == "nccl" else (2 if self.remote in ("packed", "packed_all") else 1)
 
-    def enqueue(self, stream: int) -> None:
+    def enqueue(self, stream: int, marks=None) -> None:
+        """Put the exchange on ``stream``.  ``marks`` (diagnostics): three
+        callables run between the launches of a device-synced process-mode
+        exchange (e.g. CUDA event records on ``stream``) -- before the push
+        kernel, after it, after the unpack / DONE wait."""
         if self.transport == "nccl":
             self._enqueue_nccl(stream)
         elif self.mode == "serial":
             self.b_ex.run(stream)
         elif self.mode == "process" and self.sync == "device" and self.fused:
             e = self.psync.next_epoch()
+            if marks:
+                marks[0]()
             self.b_ex.run_synced(stream, e)  # pushes wait per peer for READY, then signal DONE
+            if marks:
+                marks[1]()
             if self.unp is not None:
                 self.b_unp.run_synced(stream, e)  # each peer's slab unpacked once its DONE lands
             else:
                 self.ex.sync_wait(e, stream)  # every push into my fabs has landed
+            if marks:
+                marks[2]()
         elif self.mode == "process" and self.sync == "device":
             self.psync.barrier(stream)  # peers finished earlier work on their fabs
             self.b_ex.run(stream)

@@ -107,3 +107,5 @@ def test_our_arm_two_ranks_device_sync():
     d = json.loads(lines[0])
     assert d["config"]["sync"] == "device" and d["config"]["transport"] == "p2p"
     assert d["verified"] is True and d["e2e"]["verified"] is True
+    bd = d["multi_gpu_breakdown"]  # per-rank push and unpack kernels, max over ranks
+    assert bd["push_kernel_ms"] > 0 and bd["unpack_or_wait_ms"] > 0 and bd["remote"] == "packed"

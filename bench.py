@@ -981,10 +981,19 @@ def main():
             torch.distributed.init_process_group(backend)
     try:
         run_ours(args, cfg, rank, world)
-    finally:
+    except BaseException:
         if world > 1:
-            torch.distributed.barrier()
-            torch.distributed.destroy_process_group()
+            # never wait for the peers after a failure (they may sit in a
+            # collective or a device wait): report and leave, torchrun then
+            # tears the job down instead of hanging it
+            import traceback
+            traceback.print_exc()
+            sys.stderr.flush()
+            os._exit(1)
+        raise
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
 
 
 if __name__ == "__main__":

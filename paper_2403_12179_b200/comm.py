@@ -675,6 +675,22 @@ def _transport(ctx=None) -> str:
     return t
 
 
+def _ipc_open(device: int, handle: bytes) -> int:
+    """Map a peer's CUDA-IPC allocation.  If CUDA says the memory is already
+    mapped, a stale mapping of a freed allocation at the same address is
+    still held by objects awaiting the cyclic GC in this process (an
+    Exchange and its MultiFab reference each other): collect, which closes
+    those mappings through their finalizers, and retry once."""
+    p = C.c_void_p()
+    rc = N.lib.ghx_ipc_open_handle(device, (C.c_uint8 * 64).from_buffer_copy(handle), C.byref(p))
+    if rc != 0 and "already mapped" in N.lib.ghx_last_error().decode():
+        import gc
+        gc.collect()
+        rc = N.lib.ghx_ipc_open_handle(device, (C.c_uint8 * 64).from_buffer_copy(handle), C.byref(p))
+    N.check(rc)
+    return p.value
+
+
 def _ipc_capable(ctx) -> bool:
     """Collective probe (cached on the context): every rank exports a small
     device allocation and maps every peer's; the IPC push is used only if
@@ -697,12 +713,10 @@ def _ipc_capable(ctx) -> bool:
         if other is None:
             ok = False
             break
-        p = C.c_void_p()
         try:
             if os.environ.get("GHX_TEST_NO_IPC"):  # tests: a box without CUDA IPC between processes
                 raise N.GhostxError("CUDA IPC disabled (GHX_TEST_NO_IPC)")
-            N.check(N.lib.ghx_ipc_open_handle(ctx.device, (C.c_uint8 * 64).from_buffer_copy(other), C.byref(p)))
-            N.lib.ghx_ipc_close_handle(p)
+            N.lib.ghx_ipc_close_handle(C.c_void_p(_ipc_open(ctx.device, other)))
         except Exception:  # noqa: BLE001
             ok = False
     cap = all(ctx.allgather(ok))
@@ -717,6 +731,26 @@ def _ipc_capable(ctx) -> bool:
 
 def _host_resident(mf) -> bool:
     return getattr(mf, "memory", "device") == "pinned"
+
+
+@contextlib.contextmanager
+def torch_stream(stream: int, device: int):
+    """Make the raw CUDA stream ``stream`` torch's current stream (torch's
+    collectives and copies order against the current stream).  Handle 0 is
+    the legacy default stream, which torch knows as its default stream:
+    ``torch.cuda.ExternalStream(0)`` is NOT that stream (it syncs nothing
+    launched on 0), so 0 must map to ``torch.cuda.default_stream``."""
+    import torch
+    dev = torch.device("cuda", device)
+    cur = torch.cuda.current_stream(dev)
+    if cur.cuda_stream == stream:
+        ts = cur
+    elif stream == 0:
+        ts = torch.cuda.default_stream(dev)
+    else:
+        ts = torch.cuda.ExternalStream(stream, device=dev)
+    with torch.cuda.stream(ts):
+        yield ts
 
 
 def _stream(device: int):
@@ -761,10 +795,9 @@ class _ProcessSync:
             if r == ctx.rank:
                 self.ptrs.append(self.slab.ptr)
                 continue
-            p = C.c_void_p()
-            N.check(N.lib.ghx_ipc_open_handle(ctx.device, (C.c_uint8 * 64).from_buffer_copy(hb), C.byref(p)))
-            self.ptrs.append(p.value)
-            self._opened.append(p.value)
+            pv = _ipc_open(ctx.device, hb)
+            self.ptrs.append(pv)
+            self._opened.append(pv)
         self.table = np.asarray(self.ptrs, np.uint64)
         self.epoch = 0
 
@@ -827,10 +860,9 @@ def _ipc_peers(ctx, mf: MultiFab):
             continue
         if hb is None:
             continue
-        p = C.c_void_p()
-        N.check(N.lib.ghx_ipc_open_handle(mf.device, (C.c_uint8 * 64).from_buffer_copy(hb), C.byref(p)))
-        opened.append(p.value)
-        parts.append((idx, np.asarray([p.value + o for o in off], np.uint64)))
+        pv = _ipc_open(mf.device, hb)
+        opened.append(pv)
+        parts.append((idx, np.asarray([pv + o for o in off], np.uint64)))
     mf._peer_cache["ipc"] = parts
     weakref.finalize(mf, _close_ipc, list(opened))
     return parts
@@ -986,10 +1018,9 @@ class Exchange:
         for (r, hb, roffs, _, _) in infos:
             if r == me or self.ex.buffer_elems[r] == 0:
                 continue
-            p = C.c_void_p()
-            N.check(N.lib.ghx_ipc_open_handle(dst_mf.device, (C.c_uint8 * 64).from_buffer_copy(hb), C.byref(p)))
-            self._opened.append(p.value)
-            send[r] = p.value + roffs[me]
+            pv = _ipc_open(dst_mf.device, hb)
+            self._opened.append(pv)
+            send[r] = pv + roffs[me]
         recv = np.asarray([self._recv.ptr + o for o in offs], np.uint64)
         bufs = np.concatenate([send, recv])
         # with every remote tag packed, only this rank's own fabs are addressed
@@ -1035,17 +1066,16 @@ class Exchange:
         # torch's CURRENT stream: make ``stream`` current for the whole
         # sequence so the sends follow the pack and the unpack follows the
         # receives on the caller's stream
-        import torch
-        with torch.cuda.stream(torch.cuda.ExternalStream(stream, device=torch.device("cuda", self.device))):
-            self._enqueue_nccl_current(stream)
+        with torch_stream(stream, self.device) as ts:
+            self._enqueue_nccl_current(stream, ts)
 
-    def _enqueue_nccl_current(self, stream: int) -> None:
+    def _enqueue_nccl_current(self, stream: int, ts) -> None:
         import torch
         import torch.distributed as dist
         self.b_pack.run(stream)
         if dist.get_backend() != "nccl":
             # host-staged message passing (gloo): test path for ranks sharing a GPU
-            torch.cuda.current_stream(self.device).synchronize()
+            ts.synchronize()
             send = {r: t.cpu() for r, t in self.send_t.items()}
             recv = {r: torch.empty(t.shape, dtype=t.dtype) for r, t in self.recv_t.items()}
             ops = [dist.P2POp(dist.isend, t, r) for r, t in sorted(send.items())]

@@ -300,6 +300,10 @@ bool inside(const int64_t *outer, const int64_t *lo, const int64_t *hi) {
 
 int cuda_fail(cudaError_t e, const char *what) {
   set_error(std::string(what) + ": " + cudaGetErrorString(e));
+  // consume a non-sticky error (e.g. cudaErrorAlreadyMapped from an IPC open
+  // the caller retries) so a later cudaGetLastError() does not report it
+  // again for an unrelated, successful call
+  (void)cudaGetLastError();
   return GHX_ECUDA;
 }
 

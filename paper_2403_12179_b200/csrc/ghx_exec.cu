@@ -858,6 +858,10 @@ struct DeviceGuard {
 
 int cuda_fail(cudaError_t e, const char *what) {
   set_error(std::string(what) + ": " + cudaGetErrorString(e));
+  // consume a non-sticky error (e.g. cudaErrorAlreadyMapped from an IPC open
+  // the caller retries) so a later cudaGetLastError() does not report it
+  // again for an unrelated, successful call
+  (void)cudaGetLastError();
   return GHX_ECUDA;
 }
 

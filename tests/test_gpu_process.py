@@ -258,3 +258,30 @@ def test_parallel_copy_two_processes(env):
         p.join(timeout=120)
     for r in range(2):
         assert res[r] == 0, res[r]
+
+
+def test_torch_stream_zero_orders_against_native_launches():
+    """comm.torch_stream(0) must be torch's view of the SAME legacy default
+    stream the native library launches on when handed 0 (torch's
+    ExternalStream(0) is another stream): its synchronize waits for them."""
+    import time
+
+    import torch
+
+    import paper_2403_12179_b200 as amr
+    from paper_2403_12179_b200 import comm
+    amr.config.set_spacedim(3)
+    dom = amr.Box((0, 0, 0), (255, 255, 255))
+    geom = amr.Geometry(dom, (0.0,) * 3, (1.0,) * 3, (True,) * 3)
+    mf = amr.MultiFab(amr.decompose(dom, 64), amr.DistributionMapping.round_robin(64, 1), 4, 2, geom)
+    mf.fill_hash(1, dom)
+    x = comm.prepare_fill_boundary(mf, geom)
+    torch.cuda.synchronize()
+    with comm.torch_stream(0, 0) as ts:
+        assert ts.cuda_stream == 0
+        for _ in range(40):  # ~3.5 ms of native work on stream 0
+            x.b_ex.run(0)
+        t0 = time.perf_counter()
+        ts.synchronize()
+        waited = time.perf_counter() - t0
+    assert waited > 1e-3, waited

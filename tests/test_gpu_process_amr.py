@@ -28,8 +28,9 @@ def _g3(v, dim):
     return [v if d < dim else 0 for d in range(3)]
 
 
-def _worker(rank, world, port, q, name):
+def _worker(rank, world, port, q, name, env=None):
     try:
+        os.environ.update(env or {})
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
                           LOCAL_RANK="0")
         import torch
@@ -130,13 +131,18 @@ TWO_RANK = [n for kind in ("fill_patch", "average_down", "heat", "index_copy")
             for n in [m for m in names(kind) if case(m)["nranks"] == 2][:3]]
 
 
+ENVS = {"host-sync": {}, "devsync": {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "20"},
+        "fallback": {"GHX_TRANSPORT": "nccl"}}
+
+
+@pytest.mark.parametrize("mode", sorted(ENVS))
 @pytest.mark.parametrize("name", TWO_RANK)
-def test_level_transfers_two_processes(name):
+def test_level_transfers_two_processes(name, mode):
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q, name)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, name, ENVS[mode])) for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=600) for _ in range(world))

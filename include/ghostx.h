@@ -187,6 +187,12 @@ int ghx_exec_task_kinds(const ghx_exec *ex, int64_t out[6]);
  * of phase 2, device tags. */
 int ghx_exec_phases(const ghx_exec *ex, int64_t out[4]);
 
+/* Unpack executors of a FillBoundary: how many x-face ghost tags run as
+ * sector fills (each 16-byte ghost half stored with the valid half of its
+ * 32-byte sector, read from the same fab, so no partial-sector writes;
+ * GHX_SECTOR_FILL=0 at create time turns it off). */
+int ghx_exec_sector_fills(const ghx_exec *ex, int64_t *ntags);
+
 /* Launch-time tuning knob (warps per block * blocks): 0 = default. */
 int ghx_exec_set_grid(ghx_exec *ex, int32_t blocks, int32_t threads);
 

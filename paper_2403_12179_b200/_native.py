@@ -61,6 +61,7 @@ _SIGS = {
     "ghx_exec_set_bulk": (C.c_int, [P, I32]),
     "ghx_exec_set_sync": (C.c_int, [P, C.POINTER(P), I32, I32]),
     "ghx_exec_phases": (C.c_int, [P, PI64]),
+    "ghx_exec_sector_fills": (C.c_int, [P, PI64]),
     "ghx_exec_run_synced": (C.c_int, [P, I64, C.c_uint64, P]),
     "ghx_exec_sync_wait": (C.c_int, [P, C.c_uint64, P]),
     "ghx_arena_create": (C.c_int, [I32, I32, I32, C.c_size_t, C.POINTER(P)]),

@@ -514,6 +514,9 @@ class Executor:
         ph = np.zeros(4, np.int64)
         N.check(N.lib.ghx_exec_phases(h, N.i64p(ph)))
         self.detail["phased"] = int(ph[0])
+        sf = C.c_int64()
+        N.check(N.lib.ghx_exec_sector_fills(h, C.byref(sf)))
+        self.detail["sector_fill_tags"] = sf.value
 
     def run(self, table: np.ndarray, stream: int) -> None:
         """One launch with a raw pointer table (bound on the fly; an

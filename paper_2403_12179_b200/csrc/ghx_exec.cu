@@ -65,6 +65,9 @@ constexpr int kChunk = 32 * kU;     // vectors per chunk (a task has two)
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kSwapSlots = 8;
+// task kinds (int4 .z): >= -1 copy / pair, -2 sector swap, -3 chain, -4 ring,
+// -5 bulk rows, -6 tile ring, <= kFillTask sector fill (.z = kFillTask - mate)
+constexpr int kFillTask = -16;
 #ifndef GHX_CHAIN_ROWS
 #define GHX_CHAIN_ROWS 16
 #endif
@@ -272,6 +275,48 @@ __device__ __forceinline__ void swap_chunk(const DevTag &t, uint32_t start, int 
         const uint32_t w[8] = {lo[u].x, lo[u].y, lo[u].z, lo[u].w, hi[u].x, hi[u].y, hi[u].z, hi[u].w};
         st32(da + (vec_offset<false>(t, v) << 4), w);
         st32(sl + (vec_offset<true>(t, v) << 4), w);
+      }
+    }
+  }
+}
+
+// Sector fill (unpack of 16-byte x-ghost rows from a receive buffer): the
+// ghost half of a 32-byte sector is stored together with the sector's other
+// half -- valid cells of the same fab, which no tag writes, read first -- so
+// the sector is written whole and L2 never merges a partial sector with HBM
+// (a 16-byte ghost store costs a line fill plus a write-back; the whole
+// sector costs what a local sector swap does).  The host enables it per tag
+// when every row's vector sits in the same sector half (dst_off & 1, for a
+// 32-byte aligned fab base) and the other half is valid cells; a fab base
+// that is only 16-byte aligned runs the task as a plain copy instead.
+__device__ __forceinline__ bool fill_aligned(const DevTag &t) {
+  return ((t.dst - ((uint64_t)t.dst_off << 4)) & 31) == 0;
+}
+
+template <int LD>
+__device__ __forceinline__ void fill_chunk(const DevTag &t, uint32_t start, int lane) {
+  constexpr int kS = kU / GHX_SWAP_PASSES;
+  const char *sb = reinterpret_cast<const char *>(t.src);
+  char *db = reinterpret_cast<char *>(t.dst);
+  const bool ghost_hi = t.dst_off & 1;  // the ghost is the sector's high half
+#pragma unroll 1
+  for (int h = 0; h < GHX_SWAP_PASSES; ++h) {
+    uint4 g[kS], o[kS];
+#pragma unroll
+    for (int u = 0; u < kS; ++u) {
+      const uint32_t v = start + (uint32_t)((h * kS + u) * 32 + lane);
+      if (v < t.nvec) {
+        g[u] = ld16<LD>(sb + (vec_offset<true>(t, v) << 4));
+        o[u] = ld16<LD>(db + (vec_offset<false>(t, v) << 4) + (ghost_hi ? -16 : 16));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kS; ++u) {
+      const uint32_t v = start + (uint32_t)((h * kS + u) * 32 + lane);
+      if (v < t.nvec) {
+        const uint4 lo = ghost_hi ? o[u] : g[u], hi = ghost_hi ? g[u] : o[u];
+        const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+        st32(db + (vec_offset<false>(t, v) << 4) - (ghost_hi ? 16 : 0), w);
       }
     }
   }
@@ -672,7 +717,7 @@ __global__ void ghx_bind_kernel(DevTag *tags, int ntags, void *const *__restrict
 // per-executor counter (counter[0]); every warp counts itself out in
 // counter[1] and the last one resets both, so the next launch (stream
 // ordered) starts from zero without a memset.  Heavy tasks come first.
-template <int LD, bool RING = false, bool BULK = false>
+template <int LD, bool RING = false, bool BULK = false, bool FILL = false>
 __global__ void __launch_bounds__(kThreads, RING ? 1 : GHX_MINB) ghx_copy_kernel(const DevTag *__restrict__ tags,
                                                             const int4 *__restrict__ tasks, int ntasks,
                                                             const int *__restrict__ chains,
@@ -750,12 +795,12 @@ __global__ void __launch_bounds__(kThreads, RING ? 1 : GHX_MINB) ghx_copy_kernel
     for (int w = (int)first; w < last; ++w) {
       const int4 nxt = (w + 1 < last) ? __ldg(tasks + w + 1) : tk;
       if (phased) pass_to(w >= sync.pe1 ? 2 : (w >= sync.pe0 ? 1 : 0), true);
-      if (tk.z >= -1 && (sync.mode == 2 || (sync.mode == 1 && w < sync.nhead))) {
+      if ((tk.z >= -1 || tk.z <= kFillTask) && (sync.mode == 2 || (sync.mode == 1 && w < sync.nhead))) {
         // a remote push waits for the peer's READY, an unpack for its DONE
         // (both tags of a pair task: they may belong to different peers)
 #pragma unroll 1
         for (int k2 = 0; k2 < 2; ++k2) {
-          const int tg = k2 ? tk.z : tk.x;
+          const int tg = k2 ? (tk.z <= kFillTask ? kFillTask - tk.z : tk.z) : tk.x;
           if (tg < 0) continue;
           const int peer = __ldg(sync.tag_peer + tg);
           if (peer >= 0 && peer < 64 && !((peers_ok >> peer) & 1ull)) {
@@ -767,7 +812,7 @@ __global__ void __launch_bounds__(kThreads, RING ? 1 : GHX_MINB) ghx_copy_kernel
           }
         }
       }
-      if (tk.z == -3) {  // chain task: all seams of one chain, kChainRows rows
+      if (!FILL && tk.z == -3) {  // chain task: all seams of one chain, kChainRows rows
         chain_task<LD>(tags, chains, tk.x, tk.w, (uint32_t)tk.y, kChainRows, lane);
       } else if (RING && tk.z == -4) {  // ring task: seam chunks of 32/(2k) columns of one x-ring
         ring_task<LD>(tags, chains, tk.x, tk.w, tk.y, lane);
@@ -782,9 +827,33 @@ __global__ void __launch_bounds__(kThreads, RING ? 1 : GHX_MINB) ghx_copy_kernel
           __syncwarp();
         }
         bulk_task(ta, (uint32_t)tk.y, (uint32_t)tk.w, lane, bulk_smem + wib * kBulkBytes, &bulk_bar[wib], bulk_phase);
-      } else if (tk.z < -2) {  // a task kind this instantiation does not carry: fail loudly
+      } else if (FILL && tk.z <= kFillTask) {  // sector-fill task: chunk tk.y of tag tk.x, chunk tk.w of tag kFillTask - tk.z
+        const int bt = kFillTask - tk.z;
+        if (tk.x != have_a || (bt != tk.x && bt != have_b)) {
+          __syncwarp();
+          if (tk.x != have_a) fetch_tag(tags, tk.x, &ta, lane);
+          if (bt != tk.x && bt != have_b) fetch_tag(tags, bt, &tb, lane);
+          have_a = tk.x;
+          if (bt != tk.x) have_b = bt;
+          __syncwarp();
+        }
+        const DevTag &tB = bt == tk.x ? ta : tb;
+#pragma unroll 1
+        for (int k2 = 0; k2 < 2; ++k2) {
+          if (k2 && tk.w < 0) break;
+          const DevTag &tt = k2 ? tB : ta;
+          const uint32_t st = (uint32_t)(k2 ? tk.w : tk.y);
+          if (fill_aligned(tt)) {
+            fill_chunk<LD>(tt, st, lane);
+          } else {
+            uint4 val[kU];
+            load_chunk<LD>(tt, st, lane, val);
+            store_chunk(tt, st, lane, val);
+          }
+        }
+      } else if (tk.z < -2 || (FILL && tk.z == -2)) {  // a task kind this instantiation does not carry: fail loudly
         __trap();
-      } else if (tk.z == -2) {  // sector-swap task over one chunk of T1
+      } else if (!FILL && tk.z == -2) {  // sector-swap task over one chunk of T1
         const int sl = tk.x & (kSwapSlots - 1);
         if (swc_id[wib][sl] != tk.x) {
           __syncwarp();
@@ -890,6 +959,10 @@ struct HostTag {
   int32_t peer;            // push: destination rank of a remote tag; unpack: source rank; else -1
   int32_t sfab, dfab;      // plan fab ids (pairing)
   int64_t shift[3];
+  // sector fill (unpack of x-face ghosts): the destination's valid x range
+  // and the tag's first x, in elements from the storage box's lo (fill_vhi <
+  // fill_vlo: not eligible)
+  int64_t fill_x0 = 0, fill_vlo = 0, fill_vhi = -1;
 };
 
 int vec_log(const HostTag &t, int64_t eb, int64_t x0, int64_t nxe) {
@@ -1057,6 +1130,8 @@ struct ghx_exec {
   bool phased = false;
   int8_t cur_phase = 0;         // phase of the tag being emitted
   std::vector<int8_t> hphase;   // per tag
+  std::vector<uint8_t> hfill;   // per tag: 16-byte ghost halves written as whole sectors (fill_load)
+  int64_t nfill = 0;            // tags run as sector-fill tasks
   int32_t pe0 = 0, pe1 = 0;
   // in-kernel synchronisation (ghx_exec_set_sync)
   int32_t sync_rank = -1, sync_n = 0;
@@ -1126,6 +1201,16 @@ void add_devtag(ghx_exec *ex, const HostTag &t, int64_t x0, int64_t nxe, int vl,
   ex->hremote.push_back(t.remote ? 1 : 0);
   ex->hpeer.push_back(t.peer);
   ex->hphase.push_back(ex->cur_phase);
+  // sector fill: one 16-byte vector per row, every row in the same sector
+  // half (even strides), and the other half of its sectors valid cells
+  bool fill = t.fill_vhi >= t.fill_vlo && vl == 4 && g.nxv == 1 && g.dst_sy % 2 == 0 && g.dst_sz % 2 == 0 &&
+              g.dst_sc % 2 == 0;
+  if (fill) {
+    const int64_t x = t.fill_x0 + x0;  // first element of the vector
+    const int64_t olo = (g.dst_off & 1) ? x - epv : x + epv;
+    fill = olo >= t.fill_vlo && olo + epv - 1 <= t.fill_vhi;
+  }
+  ex->hfill.push_back(fill ? 1 : 0);
 }
 
 // Split a row range into an unaligned head, 16-byte body and tail when src
@@ -1281,6 +1366,10 @@ void build_tasks(ghx_exec *ex) {
     return ex->bulk && !ex->ring && !ex->hremote[i] && t.vlog == 4 && rb >= 256 && rb <= (uint32_t)kBulkBytes &&
            ex->kind <= GHX_EXEC_LOCAL;
   };
+  // sector fill: not over PCIe (ring executors: fabs in host memory, where
+  // the extra 16-byte read costs a request)
+  ex->nfill = 0;
+  auto fill_ok = [&](size_t i) { return !ex->ring && i < ex->hfill.size() && ex->hfill[i] && n < (1u << 30); };
   auto emit_bulk = [&](size_t i, std::vector<int4> &out) {
     const DevTag &t = ex->htags[i];
     const uint32_t rows = t.nvec / t.nxv, per = std::min<uint32_t>(32, kBulkBytes / (t.nxv << 4));
@@ -1308,9 +1397,18 @@ void build_tasks(ghx_exec *ex) {
         emit_bulk(mate[i], out);
         continue;
       }
+      if (fill_ok(i) && fill_ok(mate[i]) && ex->htags[mate[i]].nvec == nv) {
+        ex->nfill += 2;
+        for (uint32_t s = 0; s < nv; s += kChunk) out.push_back(make_int4((int)i, (int)s, kFillTask - mate[i], (int)s));
+        continue;
+      }
       for (uint32_t s = 0; s < nv; s += kChunk) out.push_back(make_int4((int)i, (int)s, mate[i], (int)s));
     } else if (bulk_ok(i)) {
       emit_bulk(i, out);
+    } else if (fill_ok(i)) {
+      ex->nfill += 1;
+      for (uint32_t s = 0; s < nv; s += 2 * kChunk)
+        out.push_back(make_int4((int)i, (int)s, kFillTask - (int)i, s + kChunk < nv ? (int)(s + kChunk) : -1));
     } else {
       for (uint32_t s = 0; s < nv; s += 2 * kChunk)
         out.push_back(make_int4((int)i, (int)s, s + kChunk < nv ? (int)i : -1, (int)(s + kChunk)));
@@ -1554,6 +1652,11 @@ int ghx_exec_create(const ghx_plan *plan, int32_t rank, int32_t kind, const int6
   auto packable = [&](const Piece &p) {
     return p.srank != p.drank && (pack_all || (p.dbox.hi[0] - p.dbox.lo[0] + 1) * elem_bytes <= pack_row_bytes);
   };
+  // sector fill for the unpack kinds of a FillBoundary (GHX_SECTOR_FILL=0: off)
+  const char *sf = std::getenv("GHX_SECTOR_FILL");
+  const bool fill_ok = (kind == GHX_EXEC_UNPACK || kind == GHX_EXEC_UNPACK_PACKED || kind == GHX_EXEC_UNPACK_PACKED_ALL) &&
+                       plan->mode == GHX_MODE_FILL_BOUNDARY && !plan->clipped &&
+                       (int64_t)plan->vbox.size() == plan->ndst && !(sf && std::atoi(sf) == 0);
   int64_t bad = -1;
   std::vector<Piece> taken;
   std::vector<int64_t> taken_id;  // wtags index (error reporting)
@@ -1655,6 +1758,18 @@ int ghx_exec_create(const ghx_plan *plan, int32_t rank, int32_t kind, const int6
       t.d.sc = cells;
       t.d.ptr = send_base + p.drank;
       buf_off[p.drank] += cells * ncomp;
+    }
+    if (fill_ok && !src_is_fab && dst_is_fab) {
+      // an x-face ghost piece (outside the valid box in x only): its sectors'
+      // other halves may be valid cells, which a FillBoundary never writes
+      const Box &V = plan->vbox[p.dst];
+      bool xface = p.dbox.hi[0] < V.lo[0] || p.dbox.lo[0] > V.hi[0];
+      for (int d = 1; d < 3; ++d) xface = xface && p.dbox.lo[d] >= V.lo[d] && p.dbox.hi[d] <= V.hi[d];
+      if (xface) {
+        t.fill_x0 = p.dbox.lo[0] - D.box.lo[0];
+        t.fill_vlo = V.lo[0] - D.box.lo[0];
+        t.fill_vhi = V.hi[0] - D.box.lo[0];
+      }
     }
     if (cells * ncomp >= (1ll << 31)) {
       set_error("ghx_exec_create: a single tag exceeds 2^31 elements");
@@ -1877,6 +1992,15 @@ int ghx_exec_phases(const ghx_exec *ex, int64_t out[4]) {
   return GHX_OK;
 }
 
+int ghx_exec_sector_fills(const ghx_exec *ex, int64_t *ntags) {
+  if (!ex || !ntags) {
+    set_error("ghx_exec_sector_fills: bad arguments");
+    return GHX_EINVAL;
+  }
+  *ntags = ex->nfill;
+  return GHX_OK;
+}
+
 int ghx_exec_buffer_elems(const ghx_exec *ex, int64_t *per_peer) {
   if (!ex || !per_peer) {
     set_error("ghx_exec_buffer_elems: bad arguments");
@@ -2020,6 +2144,9 @@ int launch(ghx_exec *ex, ghx_exec::Binding *bd, cudaStream_t st, const SyncArgs 
                                                                                         counter, batch, sy);
     else if (ring)  // ring tasks present: the ring-capable instantiation
       ghx_copy_kernel<2, true><<<nblocks, ex->threads, 0, st>>>(dtags, tk, count, ex->dchain, counter, batch, sy);
+    else if (ex->nfill)  // sector-fill tasks (unpack): their own instantiation keeps the others spill-free
+      ghx_copy_kernel<2, false, false, true><<<nblocks, ex->threads, 0, st>>>(dtags, tk, count, ex->dchain, counter,
+                                                                             batch, sy);
     else switch (ld) {
       case 0: ghx_copy_kernel<0><<<nblocks, ex->threads, 0, st>>>(dtags, tk, count, ex->dchain, counter, batch, sy); break;
       case 1: ghx_copy_kernel<1><<<nblocks, ex->threads, 0, st>>>(dtags, tk, count, ex->dchain, counter, batch, sy); break;

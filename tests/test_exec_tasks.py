@@ -161,3 +161,46 @@ def test_diagnostic_xface_split_partitions_the_exchange(n, b, nc, ng):
         N.lib.ghx_plan_free(h)
     assert elems["x"] + elems["rest"] == elems["all"] and elems["x"] > 0 and elems["rest"] > 0
     assert elems["x"] == len(boxes) * 2 * ng * b * b * nc
+
+
+def sector_fills(n, b, nc, ng, kind, item=8, env=None, ring=False, monkeypatch=None):
+    """Tags an executor of rank 0 (2 ranks, round-robin boxes) runs as sector fills."""
+    if env is not None:
+        monkeypatch.setenv("GHX_SECTOR_FILL", env)
+    boxes = gu.scale_boxes(n, b)
+    h = native_fb(boxes, [ng] * 3, [1, 1, 1], [n] * 3, [i % 2 for i in range(len(boxes))], 2)
+    storage = boxes.copy()
+    storage[:, :3] -= ng
+    storage[:, 3:] += ng
+    storage = np.ascontiguousarray(storage)
+    ex = C.c_void_p()
+    try:
+        N.check(N.lib.ghx_exec_create(h, 0, kind, N.i64p(storage), nc, N.i64p(storage), nc, 0, 0, nc, item, 0,
+                                      C.byref(ex)))
+        if ring:
+            N.check(N.lib.ghx_exec_set_ring(ex, 1))
+        v = C.c_int64()
+        N.check(N.lib.ghx_exec_sector_fills(ex, C.byref(v)))
+        return v.value
+    finally:
+        if ex:
+            N.lib.ghx_exec_free(ex)
+        N.lib.ghx_plan_free(h)
+
+
+def test_unpack_x_ghosts_run_as_sector_fills(monkeypatch):
+    # 4 x 4 x 4 boxes, ranks alternate along x: every x-face is remote.  Rank
+    # 0 receives, per fab, a lo- and a hi-x ghost tag of 16-byte rows (f64,
+    # ng 2) whose sectors' other halves are valid cells
+    assert sector_fills(64, 16, 2, 2, N.EXEC_UNPACK_PACKED) == 32 * 2
+    assert sector_fills(64, 16, 2, 2, N.EXEC_UNPACK) == 32 * 2
+    assert sector_fills(64, 16, 2, 2, N.EXEC_UNPACK_PACKED, env="0", monkeypatch=monkeypatch) == 0
+    # pushes, host-memory (ring) executors, rows that are not one 16-byte
+    # vector (ng 1: 8-byte rows; f32 ng 2: 8-byte rows) -> no fills
+    monkeypatch.delenv("GHX_SECTOR_FILL", raising=False)
+    assert sector_fills(64, 16, 2, 2, N.EXEC_PUSH_PACKED) == 0
+    assert sector_fills(64, 16, 2, 2, N.EXEC_UNPACK_PACKED, ring=True) == 0
+    assert sector_fills(64, 16, 2, 1, N.EXEC_UNPACK_PACKED) == 0
+    assert sector_fills(64, 16, 2, 2, N.EXEC_UNPACK_PACKED, item=4) == 0
+    # f32 ng 4: 16-byte rows again
+    assert sector_fills(64, 16, 2, 4, N.EXEC_UNPACK_PACKED, item=4) == 32 * 2

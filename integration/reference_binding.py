@@ -14,12 +14,24 @@ The arena duck-types the reference's (arena.py:87-163: ``alloc(nbytes,
 align)`` returning a block with ``as_array(dtype, count)`` / ``free()``),
 so Fab (mesh.py:43-86) allocates its storage in memory the GPU kernel can
 address directly (UVA: the host pointer is the device pointer).
+
+Under the reference's ``runtime_spawn`` (rank threads, comm.py:143-180)
+the same calls are collective, like the reference's: every rank runs its
+share of the plan (the tags whose source fab it owns) as one launch that
+writes its neighbours' ghost cells directly -- all fabs are pinned host
+memory of one process -- between an entry barrier (no rank writes a
+peer's ghost cells before the peer has entered the call) and the
+reference's trailing barrier; one Bus message per ordered rank pair with
+the pair's payload bytes keeps ``Bus.message_stats`` the reference's
+(comm.py:356-357).
 """
 
 from __future__ import annotations
 
 import ctypes as C
+import importlib
 import os
+import weakref
 
 import numpy as np
 
@@ -51,6 +63,9 @@ def lib():
         L.ghx_interp.argtypes = [P, I64, I32, PI32, I32, I32, I32, P]
         L.ghx_plan_build_parallel_copy.argtypes = [I64, PI64, PI64, I64, PI64, PI64, PI32, PI64, PI32, PI32, I32,
                                                    C.POINTER(P)]
+        L.ghx_plan_num_segments.argtypes = [P]
+        L.ghx_plan_num_segments.restype = I64
+        L.ghx_plan_pair_cells.argtypes = [P, PI64]
         _lib = L
     return _lib
 
@@ -125,31 +140,91 @@ def _p32(a: np.ndarray):
     return a.ctypes.data_as(PI32)
 
 
-class _Prepared:
-    """A built plan + executor for one MultiFab layout (the reference caches
-    its plan per PlanKey, comm.py:299-308; this caches both)."""
+def _ctx_of(mf):
+    """The reference's current rank context (``comm.current_ctx()`` of the
+    package the MultiFab comes from)."""
+    pkg = type(mf).__module__.rsplit(".", 1)[0]
+    return importlib.import_module(pkg + ".comm").current_ctx()
 
-    def __init__(self, mf, geom):
+
+def _allgather_addrs(ctx, local: dict) -> dict:
+    """Every rank's {fab index: address}.  Rank threads share the process, so
+    the addresses meet in a registry on the reference's Bus between two
+    barriers -- no messages, the Bus statistics stay the reference's.  The
+    n-th call on every rank uses slot n (collectives run in the same order
+    on all ranks)."""
+    if ctx.nranks == 1:
+        return dict(local)
+    reg = ctx.bus.__dict__.setdefault("_ghostx_addrs", {})
+    seq = getattr(ctx, "_ghostx_seq", 0)
+    ctx._ghostx_seq = seq + 1
+    slot = reg.setdefault(seq, {})  # atomic for a dict under the GIL
+    slot[ctx.rank] = dict(local)
+    ctx.barrier()
+    out = {}
+    for part in slot.values():
+        out.update(part)
+    ctx.barrier()  # every rank has read the slot
+    if ctx.rank == 0:
+        reg.pop(seq, None)
+    return out
+
+
+def _addrs(mf) -> dict:
+    return {i: fab.data.__array_interface__["data"][0] for i, fab in mf.fabs.items()}
+
+
+class _Prepared:
+    """A built plan + this rank's executor + its pointer table (the reference
+    caches its plan per PlanKey, comm.py:299-308; this caches all three).
+    ``plan`` is built by ``build_plan()``; the executor runs the tags whose
+    source fab this rank owns (GHX_EXEC_DIRECT), writing local and peer
+    destination fabs."""
+
+    def __init__(self, ctx, build_plan, src, dst, scomp, dcomp, ncomp, src_grow, dst_grow):
         L = lib()
-        d = len(mf.ngrow)
-        ng = np.array(list(mf.ngrow) + [0] * (3 - d), np.int64)
-        per = np.array([int(v) for v in geom.periodic] + [0] * (3 - d), np.int32)
-        period = np.array(list(geom.period) + [1] * (3 - d), np.int64)
-        rows = _rows(list(mf.ba))
-        ranks = np.asarray(mf.dm.rank_of, np.int32)
         self.plan = P()
-        _check(L.ghx_plan_build_fill_boundary(len(rows), _p64(rows), _p64(ng), _p32(per), _p64(period), _p32(ranks),
-                                              mf.dm.nranks, C.byref(self.plan)))
-        storage = _rows(list(mf.ba), grow=tuple(int(v) for v in ng))
-        item = np.dtype(mf.fabs[mf.local_indices[0]].data.dtype).itemsize
+        _check(build_plan(C.byref(self.plan)))
         self.ex = P()
-        _check(L.ghx_exec_create(self.plan, mf.rank, 0, _p64(storage), mf.ncomp, _p64(storage), mf.ncomp, 0, 0,
-                                 mf.ncomp, item, 0, C.byref(self.ex)))
-        n = len(rows)
-        self.table = np.zeros(2 * n + 2 * mf.dm.nranks, np.uint64)  # [src fabs][dst fabs][send][recv]
-        for i, fab in mf.fabs.items():
-            addr = fab.data.__array_interface__["data"][0]
-            self.table[i] = self.table[n + i] = addr
+        self.nseg = L.ghx_plan_num_segments(self.plan)
+        nranks = max(src.dm.nranks, dst.dm.nranks)
+        rank = ctx.rank
+        sst = _rows(list(src.ba), grow=src_grow)
+        dst_rows = _rows(list(dst.ba), grow=dst_grow)
+        fab = next(iter(list(dst.fabs.values()) + list(src.fabs.values())), None)
+        item = fab.data.dtype.itemsize if fab is not None else 8  # a rank without fabs runs no tags
+        _check(L.ghx_exec_create(self.plan, rank, 0, _p64(sst), src.ncomp, _p64(dst_rows), dst.ncomp, scomp, dcomp,
+                                 ncomp, item, 0, C.byref(self.ex)))
+        ns, nd = len(sst), len(dst_rows)
+        self.table = np.zeros(ns + nd + 2 * nranks, np.uint64)  # [src fabs][dst fabs][send][recv]
+        for i, a in _addrs(src).items():
+            self.table[i] = a
+        for i, a in _allgather_addrs(ctx, _addrs(dst)).items():
+            self.table[ns + i] = a
+        # Bus accounting per call: one message per ordered pair, the pair's
+        # payload bytes (the reference's pack buffers, comm.py:343-357)
+        pc = np.zeros(nranks * nranks, np.int64)
+        _check(L.ghx_plan_pair_cells(self.plan, _p64(pc)))
+        pc = pc.reshape(nranks, nranks) * ncomp * item
+        self.sends = [(d, int(pc[rank, d])) for d in range(nranks) if d != rank and pc[rank, d]]
+        self.recvs = [s for s in range(nranks) if s != rank and pc[s, rank]]
+
+    def run(self, ctx) -> None:
+        if self.nseg == 0:  # the reference returns before its barrier (comm.py:390-391)
+            return
+        L = lib()
+        multi = ctx.nranks > 1
+        if multi:
+            ctx.barrier()  # every rank is in the call: its ghost cells may be written
+        t = self.table
+        _check(L.ghx_exec_run(self.ex, t.ctypes.data_as(C.POINTER(P)), len(t), None))
+        _check(L.ghx_stream_sync(None))
+        if multi:
+            for d, nbytes in self.sends:
+                ctx.send(d, None, nbytes=nbytes)
+            for s in self.recvs:
+                ctx.recv(s)
+            ctx.barrier()
 
     def __del__(self):
         try:
@@ -160,63 +235,67 @@ class _Prepared:
 
 
 def fill_boundary_native(mf, geom=None) -> None:
-    """Drop-in body for the reference's comm.fill_boundary (comm.py:383-394)
-    on one rank: the plan and executor are built once per MultiFab and
-    geometry, every call is one kernel launch plus a stream synchronize
-    (the reference API is synchronous).  The fabs must live in device or
-    pinned-mapped memory (``PinnedArena``)."""
+    """Drop-in body for the reference's comm.fill_boundary (comm.py:383-394):
+    the plan and executor are built once per MultiFab and geometry, every
+    call is one kernel launch plus a stream synchronize (the reference API
+    is synchronous); collective under ``runtime_spawn``, where every rank
+    must build its MultiFabs at the same program points (SPMD, as the
+    reference's programs do: the first call per MultiFab is a collective
+    setup).  The fabs must live in device or pinned-mapped memory
+    (``PinnedArena``)."""
     geom = geom or mf.geom
     key = ("ghostx", id(geom))
+    ctx = _ctx_of(mf)
     prep = mf.plan_cache.get(key)
     if prep is None:
-        prep = mf.plan_cache[key] = _Prepared(mf, geom)
-    L = lib()
-    t = prep.table
-    _check(L.ghx_exec_run(prep.ex, t.ctypes.data_as(C.POINTER(P)), len(t), None))
-    _check(L.ghx_stream_sync(None))
+        L = lib()
+        d = len(mf.ngrow)
+        ng = np.array(list(mf.ngrow) + [0] * (3 - d), np.int64)
+        per = np.array([int(v) for v in geom.periodic] + [0] * (3 - d), np.int32)
+        period = np.array(list(geom.period) + [1] * (3 - d), np.int64)
+        rows = _rows(list(mf.ba))
+        ranks = np.asarray(mf.dm.rank_of, np.int32)
+
+        def build(out):
+            return L.ghx_plan_build_fill_boundary(len(rows), _p64(rows), _p64(ng), _p32(per), _p64(period),
+                                                  _p32(ranks), mf.dm.nranks, out)
+        grow = tuple(int(v) for v in ng)
+        prep = mf.plan_cache[key] = _Prepared(ctx, build, mf, mf, 0, 0, mf.ncomp, grow, grow)
+    prep.run(ctx)
 
 
 def parallel_copy_native(dst, src, scomp=0, dcomp=0, ncomp=None, ngrow_src=0, ngrow_dst=0, geom=None) -> None:
     """Drop-in body for the reference's comm.parallel_copy (comm.py:397-429)
-    on one rank (the reference's argument checks omitted): a ParallelCopy
-    plan between the two layouts and one launch over both MultiFabs'
-    fabs."""
-    L = lib()
+    (the reference's argument checks omitted): a ParallelCopy plan between
+    the two layouts, cached on ``dst`` per (source layout, ghost widths,
+    geometry), one launch per call; collective under ``runtime_spawn``."""
     ncomp = ncomp if ncomp is not None else min(src.ncomp - scomp, dst.ncomp - dcomp)
-    d = len(dst.ngrow)
-    gs = np.array([int(ngrow_src)] * d + [0] * (3 - d), np.int64)
-    gd = np.array([int(ngrow_dst)] * d + [0] * (3 - d), np.int64)
-    drows, srows = _rows(list(dst.ba)), _rows(list(src.ba))
-    if geom is not None:
-        per = np.array([int(v) for v in geom.periodic] + [0] * (3 - d), np.int32)
-        period = np.array(list(geom.period) + [1] * (3 - d), np.int64)
-        per_p, period_p = _p32(per), _p64(period)
-    else:
-        period = np.ones(3, np.int64)
-        per_p, period_p = None, _p64(period)
-    sr, dr = np.asarray(src.dm.rank_of, np.int32), np.asarray(dst.dm.rank_of, np.int32)
-    plan = P()
-    _check(L.ghx_plan_build_parallel_copy(len(drows), _p64(drows), _p64(gd), len(srows), _p64(srows), _p64(gs),
-                                          per_p, period_p, _p32(sr), _p32(dr), dst.dm.nranks, C.byref(plan)))
-    ex = P()
-    try:
-        sst = _rows(list(src.ba), grow=tuple(int(v) for v in src.ngrow) + (0,) * (3 - d))
-        dst_st = _rows(list(dst.ba), grow=tuple(int(v) for v in dst.ngrow) + (0,) * (3 - d))
-        item = dst.fabs[dst.local_indices[0]].data.dtype.itemsize
-        _check(L.ghx_exec_create(plan, dst.rank, 0, _p64(sst), src.ncomp, _p64(dst_st), dst.ncomp, scomp, dcomp,
-                                 ncomp, item, 0, C.byref(ex)))
-        ns, nd = len(srows), len(drows)
-        table = np.zeros(ns + nd + 2 * dst.dm.nranks, np.uint64)
-        for i, fab in src.fabs.items():
-            table[i] = fab.data.__array_interface__["data"][0]
-        for i, fab in dst.fabs.items():
-            table[ns + i] = fab.data.__array_interface__["data"][0]
-        _check(L.ghx_exec_run(ex, table.ctypes.data_as(C.POINTER(P)), len(table), None))
-        _check(L.ghx_stream_sync(None))
-    finally:
-        if ex:
-            L.ghx_exec_free(ex)
-        L.ghx_plan_free(plan)
+    ctx = _ctx_of(dst)
+    key = ("ghostx_pc", id(src), int(ngrow_src), int(ngrow_dst), id(geom), scomp, dcomp, ncomp)
+    prep = dst.plan_cache.get(key)
+    if prep is None or prep.src() is not src:  # (a new source at a recycled id: rebuild)
+        L = lib()
+        d = len(dst.ngrow)
+        gs = np.array([int(ngrow_src)] * d + [0] * (3 - d), np.int64)
+        gd = np.array([int(ngrow_dst)] * d + [0] * (3 - d), np.int64)
+        drows, srows = _rows(list(dst.ba)), _rows(list(src.ba))
+        if geom is not None:
+            per = np.array([int(v) for v in geom.periodic] + [0] * (3 - d), np.int32)
+            period = np.array(list(geom.period) + [1] * (3 - d), np.int64)
+        else:
+            per, period = None, np.ones(3, np.int64)
+        sr, dr = np.asarray(src.dm.rank_of, np.int32), np.asarray(dst.dm.rank_of, np.int32)
+        nranks = max(src.dm.nranks, dst.dm.nranks)
+
+        def build(out):
+            return L.ghx_plan_build_parallel_copy(len(drows), _p64(drows), _p64(gd), len(srows), _p64(srows),
+                                                  _p64(gs), None if per is None else _p32(per), _p64(period),
+                                                  _p32(sr), _p32(dr), nranks, out)
+        sg = tuple(int(v) for v in src.ngrow) + (0,) * (3 - d)
+        dg = tuple(int(v) for v in dst.ngrow) + (0,) * (3 - d)
+        prep = dst.plan_cache[key] = _Prepared(ctx, build, src, dst, scomp, dcomp, ncomp, sg, dg)
+        prep.src = weakref.ref(src)
+    prep.run(ctx)
 
 
 def interp_box_native(coarse_fab, fine_fab, fine_region, ratio: int, scheme: str = "pc") -> None:

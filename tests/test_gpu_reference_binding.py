@@ -103,3 +103,94 @@ def test_parallel_copy_through_c_abi_equals_reference(ref, n, sb, db, nc, gs, gd
     comm.parallel_copy(dst_r, src_r, 0, 1, nc, gs, gd, geom, backend=ref[0]._serial)
     for i in dst_o.local_indices:
         assert np.array_equal(dst_o.fabs[i].data.view(np.uint64), dst_r.fabs[i].data.view(np.uint64)), f"fab {i}"
+
+
+def _fill_by_fab(mf, seed):
+    """Rank-independent data: fab i's values depend on (seed, i) only."""
+    for i in mf.local_indices:
+        a = mf.fabs[i].data
+        a[...] = np.random.default_rng(seed * 1000 + i).standard_normal(a.shape)
+
+
+def _spawn(comm, nranks, program):
+    """runtime_spawn(program) -> (per-rank results, the Bus message stats)."""
+    stats = {}
+
+    def prog(ctx):
+        out = program(ctx)
+        ctx.barrier()
+        if ctx.rank == 0:
+            stats.update(ctx.bus.stats_snapshot())
+        return out
+    return comm.runtime_spawn(nranks, prog), stats
+
+
+@pytest.mark.parametrize("nranks", [2, 3, 4])
+@pytest.mark.parametrize("dim,n,b,nc,ng,per", [(3, 32, 16, 2, 2, (1, 1, 1)), (3, 24, 8, 1, 1, (1, 0, 1)),
+                                                (2, 40, 16, 3, 2, (1, 1))])
+def test_fill_boundary_rank_threads_through_c_abi_equal_reference(ref, nranks, dim, n, b, nc, ng, per):
+    """The reference's runtime_spawn rank threads, each calling the binding
+    collectively: ghost cells AND Bus message statistics equal the
+    reference's own fill_boundary on twin MultiFabs."""
+    _, _, comm, config, ix, mesh = ref
+    from integration.reference_binding import PinnedArena, fill_boundary_native
+    config.set_spacedim(dim) if hasattr(config, "set_spacedim") else None
+    dom = ix.Box((0,) * dim, (n - 1,) * dim)
+    geom = ix.Geometry(dom, (0.0,) * dim, (1.0,) * dim, per)
+    ba = mesh.decompose(dom, b)
+    dm = mesh.DistributionMapping.round_robin(len(ba), nranks)
+
+    def run(native):
+        def program(ctx):
+            mf = mesh.MultiFab(ba, dm, nc, ng, geom, arena=PinnedArena() if native else None)
+            _fill_by_fab(mf, 5)
+            for _ in range(2):
+                if native:
+                    fill_boundary_native(mf, geom)
+                else:
+                    comm.fill_boundary(mf, geom, backend=ref[0]._serial)
+            return {i: mf.fabs[i].data.copy() for i in mf.local_indices}
+        return _spawn(comm, nranks, program)
+
+    got, got_stats = run(True)
+    exp, exp_stats = run(False)
+    assert got_stats == exp_stats and any(v[0] for k, v in exp_stats.items() if k[0] != k[1])
+    for r in range(nranks):
+        assert got[r].keys() == exp[r].keys()
+        for i in got[r]:
+            assert np.array_equal(got[r][i].view(np.uint64), exp[r][i].view(np.uint64)), f"rank {r} fab {i}"
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+@pytest.mark.parametrize("n,sb,db,nc,gs,gd,periodic", [(32, 8, 16, 2, 0, 0, None), (24, 12, 8, 1, 1, 2, (1, 1, 1))])
+def test_parallel_copy_rank_threads_through_c_abi_equal_reference(ref, nranks, n, sb, db, nc, gs, gd, periodic):
+    _, _, comm, config, ix, mesh = ref
+    from integration.reference_binding import PinnedArena, parallel_copy_native
+    config.set_spacedim(3)
+    dom = ix.Box((0, 0, 0), (n - 1,) * 3)
+    geom = ix.Geometry(dom, (0.0,) * 3, (1.0,) * 3, periodic) if periodic else None
+    sba, dba = mesh.decompose(dom, sb), mesh.decompose(dom, db)
+    sdm = mesh.DistributionMapping.round_robin(len(sba), nranks)
+    ddm = mesh.DistributionMapping.round_robin(len(dba), nranks)
+
+    def run(native):
+        def program(ctx):
+            arena = PinnedArena() if native else None
+            src = mesh.MultiFab(sba, sdm, nc, gs, arena=arena)
+            dst = mesh.MultiFab(dba, ddm, nc + 1, gd, arena=arena)
+            _fill_by_fab(src, 11)
+            _fill_by_fab(dst, 12)
+            for _ in range(2):
+                if native:
+                    parallel_copy_native(dst, src, 0, 1, nc, gs, gd, geom)
+                else:
+                    comm.parallel_copy(dst, src, 0, 1, nc, gs, gd, geom, backend=ref[0]._serial)
+            return {i: dst.fabs[i].data.copy() for i in dst.local_indices}
+        return _spawn(comm, nranks, program)
+
+    got, got_stats = run(True)
+    exp, exp_stats = run(False)
+    assert got_stats == exp_stats
+    for r in range(nranks):
+        for i in got[r]:
+            assert np.array_equal(got[r][i].view(np.uint64), exp[r][i].view(np.uint64)), f"rank {r} fab {i}"

@@ -9,8 +9,11 @@ cut into 64^3 boxes, ncomp 4, float64; the fine level refines the central
 128^3 coarse cells by 2 (a 256^3 fine patch of 64 boxes of 64^3, nghost 2).
 fill_patch is LINEAR.  One JSON line per op: whole-call time (CUDA events
 around the public call, L2 flushed before each step), the dominant kernel's
-event time against the measured HBM copy bandwidth, and the numpy oracle of
-the reference arithmetic timed on a sample on the host.
+event time against the measured HBM copy bandwidth, the numpy oracle of
+the reference arithmetic timed on a sample on the host, and the reference's
+OWN public call on the same full workload (``reference_cpu``: miniamr_core
+from baseline/_ref, Backend("parallel", all host cores); GHX_AMR_NO_REF=1
+skips it).
 """
 
 from __future__ import annotations
@@ -71,6 +74,100 @@ def timed(fn, steps, warmup, flush, clean):
     return statistics.mean(ts), min(ts)
 
 
+def reference_leg(op, seconds=20.0, max_reps=20):
+    """The reference's OWN level transfer on the same workload, on the host
+    cores: miniamr_core (baseline/_ref) with Backend("parallel",
+    os.cpu_count()), its public amr.fill_patch / amr.average_down, and for
+    the heat ops its demo loop body (comm.fill_boundary + heat._advance_level
+    [+ fill_patch + average_down], reference core/heat.py:264-273).  Valid
+    cells: the splitmix64 hash of oracle/inputs.py.  The first call builds
+    the plans (reported separately); then timed calls (perf_counter) until
+    ``seconds`` or ``max_reps``, at least 2.  Returns (seconds per call,
+    dict) or (None, reason)."""
+    ref, where = bench.import_reference()
+    if ref is None:
+        return None, "reference package not importable (baseline/_ref missing)"
+    from concurrent.futures import ThreadPoolExecutor
+    from miniamr_core import amr as ramr, comm as rcomm, config as rconfig, heat as rheat
+    from miniamr_core.index_space import Box as RBox, Geometry as RGeometry
+    from miniamr_core.kernels import Backend
+    from miniamr_core.mesh import DistributionMapping as RDM, MultiFab as RMF, decompose as rdecompose
+    from oracle import inputs
+    rconfig.set_spacedim(3)
+    rconfig.set_real_dtype(np.float64)
+    cdom = RBox((0, 0, 0), (N_CRSE - 1,) * 3)
+    cgeom = RGeometry(cdom, (0.0,) * 3, (1.0,) * 3, (True,) * 3)
+    fgeom = cgeom.refined(RATIO)
+    cba = rdecompose(cdom, BOX)
+    fba = rdecompose(RBox((PATCH_LO * RATIO,) * 3, ((PATCH_HI + 1) * RATIO - 1,) * 3), BOX)
+    backend = Backend("parallel", os.cpu_count())
+    pool = ThreadPoolExecutor(os.cpu_count() or 1)
+
+    def mf(ba, geom, nc, ng):
+        m = RMF(ba, RDM.round_robin(len(ba), 1), nc, ng, geom)
+        dlo, dhi = list(geom.domain.lo), list(geom.domain.hi)
+
+        def one(gi):
+            f = m.fabs[gi]
+            inputs.fill_fab(f.data, list(f.box.lo), list(ba[gi].lo), list(ba[gi].hi), dlo, dhi)
+        list(pool.map(one, m.local_indices))
+        return m
+
+    dt, kappa = 1e-6, 1.0
+    if op == "fill_patch":
+        coarse, fine = mf(cba, cgeom, NCOMP, 0), mf(fba, fgeom, NCOMP, NGROW)
+        call = lambda: ramr.fill_patch(fine, coarse, fgeom, cgeom, RATIO, ramr.LINEAR, backend=backend)  # noqa: E731
+    elif op == "average_down":
+        coarse, fine = mf(cba, cgeom, NCOMP, 0), mf(fba, fgeom, NCOMP, NGROW)
+        call = lambda: ramr.average_down(fine, coarse, RATIO, backend)  # noqa: E731
+    elif op == "heat":
+        u, w = mf(cba, cgeom, 1, 1), mf(cba, cgeom, 1, 1)
+
+        def call():
+            rcomm.fill_boundary(u, cgeom, backend=backend)
+            rheat._advance_level(u, w, dt, kappa, cgeom, backend)
+    else:  # heat2: the two-level step
+        lv = [(mf(cba, cgeom, 1, 1), mf(cba, cgeom, 1, 1)), (mf(fba, fgeom, 1, 1), mf(fba, fgeom, 1, 1))]
+        geoms = [cgeom, fgeom]
+
+        def call():
+            rcomm.fill_boundary(lv[0][0], cgeom, backend=backend)
+            ramr.fill_patch(lv[1][0], lv[0][0], fgeom, cgeom, RATIO, ramr.LINEAR, backend=backend)
+            for k, (u, w) in enumerate(lv):
+                rheat._advance_level(u, w, dt, kappa, geoms[k], backend)
+            ramr.average_down(lv[1][1], lv[0][1], RATIO, backend)
+    pool.shutdown()
+    t0 = time.perf_counter()
+    call()  # plans built and cached, pages touched
+    first = time.perf_counter() - t0
+    times, t_end = [], time.perf_counter() + seconds
+    while len(times) < 2 or (time.perf_counter() < t_end and len(times) < max_reps):
+        a = time.perf_counter()
+        call()
+        times.append(time.perf_counter() - a)
+    t = statistics.median(times)
+    return t, {"kind": "reference", "cores": backend.nworkers, "reps": len(times),
+               "ms_per_call": round(t * 1e3, 2), "first_call_s": round(first, 3), "where": where,
+               "sample": "the full workload through the reference's public call (miniamr_core from baseline/_ref, "
+                         f"Backend('parallel', {backend.nworkers})), same layout, splitmix64 valid cells; median "
+                         f"of {len(times)} calls after the plan-building first call",
+               "cpu_model": bench.cpu_model()}
+
+
+def attach_reference(out, op, work):
+    """Add the reference's timing on the same metric to the line."""
+    if os.environ.get("GHX_AMR_NO_REF"):
+        return
+    t, info = reference_leg(op)
+    if t is None:
+        out["reference_cpu"] = {"unavailable": info}
+        return
+    info["value"] = round(work / t / (1e9 if out["unit"] in ("GB/s", "Gcell/s") else 1), 4)
+    info["unit"] = out["unit"]
+    out["reference_cpu"] = info
+    out["speedup_vs_reference"] = round(out["value"] / info["value"], 1) if info["value"] else None
+
+
 def run(args):
     import torch
     import paper_2403_12179_b200 as amr
@@ -120,6 +217,7 @@ def run(args):
                              "frac": round(alg / k_mean / 1e9 / hbm, 4), "unit": "GB/s", "peak_source": peak_src,
                              "kernel_ms": round(k_mean * 1e3, 4)})
         out["cpu_baseline"] = bench.cpu_sample_interp(fine, targets, NCOMP, NGROW, RATIO)
+        attach_reference(out, "fill_patch", ghost_bytes)
     else:
         crse_fine = amr.MultiFab(cba, amr.DistributionMapping([0] * len(cba)), NCOMP, 0, cgeom)
         call = lambda: A.average_down(fine, crse_fine, RATIO)  # noqa: E731
@@ -139,10 +237,13 @@ def run(args):
                              "frac": round(alg / k_mean / 1e9 / hbm, 4), "unit": "GB/s", "peak_source": peak_src,
                              "kernel_ms": round(k_mean * 1e3, 4)})
         out["cpu_baseline"] = bench.cpu_sample_restrict(BOX, NGROW, NCOMP, RATIO)
+        attach_reference(out, "average_down", fine_cells * NCOMP * item)
     if args.op == "heat":
         out.update(heat_bench(args, amr, cdom, cgeom, cba, flush, clean, hbm, peak_src))
+        attach_reference(out, "heat", sum(b.num_pts for b in cba))
     if args.op == "heat2":
         out.update(heat2_bench(args, amr, cdom, cgeom, cba, fba, fgeom, flush, clean))
+        attach_reference(out, "heat2", sum(b.num_pts for b in cba) + sum(b.num_pts for b in fba))
     out["amr_launches"] = int(N.lib.ghx_amr_launch_count())
     print(json.dumps(out), flush=True)
 

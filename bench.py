@@ -770,6 +770,12 @@ def run_ours(args, cfg, rank, world):
     # e2e through the public API on host-resident fabs
     if not args.no_e2e:
         line["e2e"] = e2e_leg(args, amr, cfg, L, world, ghost_bytes, x)
+        if world == 1 and cfg["kind"] == "fb" and not os.environ.get("GHX_BENCH_NO_BINDING"):
+            try:
+                line["e2e"]["reference_binding"] = e2e_binding_leg(cfg, L, mf, ghost_bytes,
+                                                                   max(1, min(args.e2e_steps, args.steps)))
+            except Exception as e:  # noqa: BLE001 - report, do not lose the GPU line
+                line["e2e"]["reference_binding"] = {"error": repr(e)[:300]}
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
             cb = reference_baseline(cfg, 1, ghost_bytes, seconds=args.cpu_seconds, keep=True)
@@ -931,6 +937,61 @@ def e2e_leg(args, amr, cfg, L, world, ghost_bytes, x):
     return {"value": round(ghost_bytes / t / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": int(moved),
             "d2h_bytes_per_step": int(moved), "ms_per_step": round(t * 1e3, 3), "steps": steps,
             "verified": verified, "path": path, "exec": x_host_detail(cfg, L, hmf, hsrc)}
+
+
+def e2e_binding_leg(cfg, L, mf, ghost_bytes, steps):
+    """The same exchange through the reference-facing C ABI: the REFERENCE's
+    own MultiFab (miniamr_core from baseline/_ref) with its numpy fabs in
+    pinned, mapped memory (integration/reference_binding.PinnedArena), and
+    integration/reference_binding.fill_boundary_native -- ctypes and
+    libghostx.so only, no torch and none of this package's Python layer on
+    the call path.  Every fab is compared with the device run's result."""
+    ref, where = import_reference()
+    if ref is None:
+        return {"unavailable": "reference package not importable (baseline/_ref missing)"}
+    need, ram = reference_bytes(cfg), _host_ram_bytes()
+    if ram is not None and need > 0.6 * ram:
+        return {"unavailable": f"needs {need / 1e9:.1f} GB pinned host memory, {ram / 1e9:.1f} GB free"}
+    from concurrent.futures import ThreadPoolExecutor
+    from miniamr_core import config as rconfig
+    from miniamr_core.index_space import Box as RBox, Geometry as RGeometry
+    from miniamr_core.mesh import DistributionMapping as RDM, MultiFab as RMF, decompose as rdecompose
+    from integration.reference_binding import PinnedArena, fill_boundary_native
+    from oracle import inputs
+    import torch
+    rconfig.set_spacedim(3)
+    rconfig.set_real_dtype(np.float64)
+    ext = cfg["ext"]
+    dom = RBox((0, 0, 0), tuple(e - 1 for e in ext))
+    geom = RGeometry(dom, (0.0,) * 3, (1.0,) * 3, (True,) * 3)
+    ba = rdecompose(dom, cfg["box"])
+    rmf = RMF(ba, RDM.round_robin(len(ba), 1), cfg["ncomp"], cfg["ngrow"], geom, arena=PinnedArena())
+    dlo, dhi = [0, 0, 0], [e - 1 for e in ext]
+
+    def one(gi):
+        f = rmf.fabs[gi]
+        inputs.fill_fab(f.data, list(f.box.lo), list(ba[gi].lo), list(ba[gi].hi), dlo, dhi)
+    with ThreadPoolExecutor(os.cpu_count() or 1) as pool:
+        list(pool.map(one, rmf.local_indices))
+    t0 = time.perf_counter()
+    fill_boundary_native(rmf, geom)  # plan + executor (cached on the MultiFab) + first exchange
+    first = time.perf_counter() - t0
+    ts = []
+    for _ in range(steps):
+        a = time.perf_counter()
+        fill_boundary_native(rmf, geom)
+        ts.append(time.perf_counter() - a)
+    t = statistics.median(ts)
+    ok = True
+    for gi in rmf.local_indices:
+        ours = mf.fabs[gi].raw().view(torch.int64).cpu().numpy()
+        theirs = rmf.fabs[gi].data.reshape(-1, order="F").view(np.int64)
+        ok = ok and bool(np.array_equal(ours, theirs))
+    return {"value": round(ghost_bytes / t / 1e9, 3), "unit": "GB/s", "ms_per_step": round(t * 1e3, 3),
+            "steps": steps, "first_call_s": round(first, 3), "verified": ok,
+            "path": "integration/reference_binding.fill_boundary_native on the reference's own MultiFab "
+                    "(miniamr_core, numpy fabs in pinned mapped memory via PinnedArena): ctypes -> libghostx.so "
+                    "(phased exchange, tile-ring seams, 8-CTA grid), every fab equal to the device run's"}
 
 
 def main():

@@ -63,6 +63,7 @@ def lib():
         L.ghx_exec_run.argtypes = [P, C.POINTER(P), I64, P]
         L.ghx_stream_sync.argtypes = [P]
         L.ghx_interp.argtypes = [P, I64, I32, PI32, I32, I32, I32, P]
+        L.ghx_average_down.argtypes = [P, I64, I32, PI32, I32, I32, P]
         L.ghx_plan_build_parallel_copy.argtypes = [I64, PI64, PI64, I64, PI64, PI64, PI32, PI64, PI32, PI32, I32,
                                                    C.POINTER(P)]
         L.ghx_plan_num_segments.argtypes = [P]
@@ -227,6 +228,20 @@ def _addrs(mf) -> dict:
     return {i: fab.data.__array_interface__["data"][0] for i, fab in mf.fabs.items()}
 
 
+class _Side:
+    """One side of an exchange: the fabs' storage boxes (int64[n, 6]), their
+    component count, this rank's {fab id: address} and the rank count."""
+
+    def __init__(self, rows, ncomp, addrs, nranks, item=None):
+        self.rows, self.ncomp, self.addrs, self.nranks, self.item = rows, int(ncomp), addrs, int(nranks), item
+
+
+def _side_of(mf, grow) -> _Side:
+    fab = next(iter(mf.fabs.values()), None)
+    return _Side(_rows(list(mf.ba), grow=grow), mf.ncomp, _addrs(mf), mf.dm.nranks,
+                 fab.data.dtype.itemsize if fab is not None else None)
+
+
 class _Prepared:
     """A built plan + this rank's executor + its pointer table (the reference
     caches its plan per PlanKey, comm.py:299-308; this caches all three).
@@ -234,33 +249,30 @@ class _Prepared:
     source fab this rank owns (GHX_EXEC_DIRECT), writing local and peer
     destination fabs."""
 
-    def __init__(self, ctx, build_plan, src, dst, scomp, dcomp, ncomp, src_grow, dst_grow):
+    def __init__(self, ctx, build_plan, src: _Side, dst: _Side, scomp, dcomp, ncomp, phased=False):
         L = lib()
         self.plan = P()
         _check(build_plan(C.byref(self.plan)))
         self.ex = P()
         self.nseg = L.ghx_plan_num_segments(self.plan)
-        nranks = max(src.dm.nranks, dst.dm.nranks)
+        nranks = max(src.nranks, dst.nranks)
         rank = ctx.rank
-        sst = _rows(list(src.ba), grow=src_grow)
-        dst_rows = _rows(list(dst.ba), grow=dst_grow)
-        fab = next(iter(list(dst.fabs.values()) + list(src.fabs.values())), None)
-        item = fab.data.dtype.itemsize if fab is not None else 8  # a rank without fabs runs no tags
+        item = dst.item or src.item or 8  # a rank without fabs runs no tags
         # the reference's fabs are numpy arrays, i.e. host memory (pinned and
         # mapped): the exchange crosses PCIe, where requests, not bytes,
         # cost -- the phased FillBoundary (faces extended over the lower-axis
         # ghosts, no edge/corner requests), seam-chunk ring tasks and a small
         # grid (include/ghostx.h)
-        kind = GHX_EXEC_DIRECT | (GHX_EXEC_PHASED if src is dst else 0)
-        _check(L.ghx_exec_create(self.plan, rank, kind, _p64(sst), src.ncomp, _p64(dst_rows), dst.ncomp, scomp,
+        kind = GHX_EXEC_DIRECT | (GHX_EXEC_PHASED if phased else 0)
+        _check(L.ghx_exec_create(self.plan, rank, kind, _p64(src.rows), src.ncomp, _p64(dst.rows), dst.ncomp, scomp,
                                  dcomp, ncomp, item, 0, C.byref(self.ex)))
         _check(L.ghx_exec_set_ring(self.ex, 1))
         _check(L.ghx_exec_set_grid(self.ex, 8, 256))
-        ns, nd = len(sst), len(dst_rows)
+        ns, nd = len(src.rows), len(dst.rows)
         self.table = np.zeros(ns + nd + 2 * nranks, np.uint64)  # [src fabs][dst fabs][send][recv]
-        for i, a in _addrs(src).items():
+        for i, a in src.addrs.items():
             self.table[i] = a
-        for i, a in _allgather_addrs(ctx, _addrs(dst)).items():
+        for i, a in _allgather_addrs(ctx, dst.addrs).items():
             self.table[ns + i] = a
         # Bus accounting per call: one message per ordered pair, the pair's
         # payload bytes (the reference's pack buffers, comm.py:343-357)
@@ -305,7 +317,7 @@ def fill_boundary_native(mf, geom=None) -> None:
     setup).  The fabs must live in device or pinned-mapped memory
     (``PinnedArena``)."""
     geom = geom or mf.geom
-    key = ("ghostx", id(geom))
+    key = ("ghostx", tuple(bool(v) for v in geom.periodic), tuple(geom.period))  # cf. PlanKey, comm.py:296-299
     ctx = _ctx_of(mf)
     prep = mf.plan_cache.get(key)
     if prep is None:
@@ -320,8 +332,9 @@ def fill_boundary_native(mf, geom=None) -> None:
         def build(out):
             return L.ghx_plan_build_fill_boundary(len(rows), _p64(rows), _p64(ng), _p32(per), _p64(period),
                                                   _p32(ranks), mf.dm.nranks, out)
-        grow = tuple(int(v) for v in ng)
-        prep = mf.plan_cache[key] = _Prepared(ctx, build, mf, mf, 0, 0, mf.ncomp, grow, grow)
+        side = _side_of(mf, tuple(int(v) for v in ng))
+        prep = mf.plan_cache[key] = _Prepared(ctx, build, side, side, 0, 0, mf.ncomp, phased=True)
+        mf.plan_builds += 1  # the reference counts its plan builds (comm.py:308)
     prep.run(ctx)
 
 
@@ -354,9 +367,156 @@ def parallel_copy_native(dst, src, scomp=0, dcomp=0, ncomp=None, ngrow_src=0, ng
                                                   _p32(sr), _p32(dr), nranks, out)
         sg = tuple(int(v) for v in src.ngrow) + (0,) * (3 - d)
         dg = tuple(int(v) for v in dst.ngrow) + (0,) * (3 - d)
-        prep = dst.plan_cache[key] = _Prepared(ctx, build, src, dst, scomp, dcomp, ncomp, sg, dg)
+        prep = dst.plan_cache[key] = _Prepared(ctx, build, _side_of(src, sg), _side_of(dst, dg), scomp, dcomp, ncomp)
         prep.src = weakref.ref(src)
+        dst.plan_builds += 1  # (comm.py:424)
     prep.run(ctx)
+
+
+def _ref_module(obj, name):
+    """A module of the reference package ``obj`` comes from."""
+    return importlib.import_module(type(obj).__module__.rsplit(".", 1)[0] + "." + name)
+
+
+class _FillPatch:
+    """fill_patch's cached coarse side for one (fine, coarse) pair: the
+    reference's own coarse-fill targets (amr.py:320-352, host planning), a
+    ParallelCopy-shaped gather plan from the coarse valid cells (periodic
+    images included) into pinned target fabs (comm.py:432-443), and one
+    interp job per (owned target, region)."""
+
+    def __init__(self, ctx, fine, coarse, fine_geom, coarse_geom, ratio, scheme):
+        ramr, rix, rmesh = (_ref_module(fine, m) for m in ("amr", "index_space", "mesh"))
+        L = lib()
+        self.coarse = weakref.ref(coarse)
+        reach = 1 if scheme == ramr.LINEAR else 0
+        targets = ramr._coarse_fill_targets(fine.ba, fine.ngrow, fine_geom)
+        gather = [(gi, rix.grow(rix.coarsen(rix.grow(fine.ba[gi], fine.ngrow), ratio), reach))
+                  for gi in sorted(targets)]
+        self.gather, self.jobs = None, None
+        if not gather:
+            return
+        me = ctx.rank
+        dst_ranks = np.asarray([fine.dm[gi] for gi, _ in gather], np.int32)
+        arena = fine.arena if isinstance(fine.arena, PinnedArena) else PinnedArena()
+        # this rank's target fabs, kept across calls (the reference allocates
+        # them per call, amr.py:385-386); plan positions address them
+        self.owned = {pos: rmesh.Fab(cbox, fine.ncomp, arena) for pos, (gi, cbox) in enumerate(gather)
+                      if dst_ranks[pos] == me}
+        d = len(fine.ngrow)
+        drows = _rows([b for _, b in gather])
+        srows = _rows(list(coarse.ba))
+        zero = np.zeros(3, np.int64)
+        per = np.array([int(v) for v in coarse_geom.periodic] + [0] * (3 - d), np.int32)
+        period = np.array(list(coarse_geom.period) + [1] * (3 - d), np.int64)
+        sr = np.asarray(coarse.dm.rank_of, np.int32)
+        nranks = max(coarse.dm.nranks, int(dst_ranks.max()) + 1)
+
+        def build(out):
+            return L.ghx_plan_build_parallel_copy(len(drows), _p64(drows), _p64(zero), len(srows), _p64(srows),
+                                                  _p64(zero), _p32(per), _p64(period), _p32(sr), _p32(dst_ranks),
+                                                  nranks, out)
+        cg = tuple(int(v) for v in coarse.ngrow) + (0,) * (3 - d)
+        item = next(iter(fine.fabs.values())).data.dtype.itemsize if fine.fabs else None
+        tside = _Side(drows, fine.ncomp, {pos: f.data.__array_interface__["data"][0] for pos, f in self.owned.items()},
+                      nranks, item)
+        self.gather = _Prepared(ctx, build, _side_of(coarse, cg), tside, 0, 0, coarse.ncomp)
+        # interp jobs (ghx_interp_job: 20 int64 words each), fine fabs in order
+        rows = []
+        pos_of = {gi: pos for pos, (gi, _) in enumerate(gather)}
+        fg = tuple(int(v) for v in fine.ngrow) + (0,) * (3 - d)
+        for gi in sorted(targets):
+            pos = pos_of[gi]
+            if pos not in self.owned:
+                continue
+            crse = self.owned[pos]
+            for region in targets[gi]:
+                rows.append([crse.data.__array_interface__["data"][0], *_rows([gather[pos][1]])[0],
+                             fine.fabs[gi].data.__array_interface__["data"][0], *_rows([fine.ba[gi]], grow=fg)[0],
+                             *_rows([region])[0]])
+        self.jobs = np.ascontiguousarray(np.asarray(rows, np.int64).reshape(-1, 20))
+        self.ratio = np.array([int(ratio)] * d + [1] * (3 - d), np.int32)
+        self.dim, self.scheme = d, 1 if scheme == ramr.LINEAR else 0
+        self.ncomp, self.item = fine.ncomp, item or 8
+
+    def run(self, ctx) -> None:
+        if self.gather is None:
+            return
+        self.gather.run(ctx)  # collective, ends with the reference's barrier
+        if len(self.jobs):
+            L = lib()
+            _check(L.ghx_interp(P(self.jobs.ctypes.data), len(self.jobs), self.ncomp, _p32(self.ratio), self.dim,
+                                self.scheme, self.item, None))
+            _check(L.ghx_stream_sync(None))
+
+
+def fill_patch_native(fine, coarse, fine_geom, coarse_geom, ratio: int, scheme: str = "linear") -> None:
+    """Drop-in body for the reference's amr.fill_patch (amr.py:355-397): the
+    fine FillBoundary, the gather of coarse data into target fabs and every
+    interpolation job in one launch; the coarse-side plan is built once per
+    (fine, coarse) pair.  Collective under ``runtime_spawn`` (SPMD)."""
+    ratio = int(ratio)
+    fill_boundary_native(fine, fine_geom)
+    ctx = _ctx_of(fine)
+    key = ("ghostx_fp", id(coarse), tuple(coarse_geom.period), ratio, scheme)
+    prep = fine.plan_cache.get(key)
+    if prep is None or prep.coarse() is not coarse:
+        prep = fine.plan_cache[key] = _FillPatch(ctx, fine, coarse, fine_geom, coarse_geom, ratio, scheme)
+        fine.plan_builds += 1  # (amr.py:380)
+    prep.run(ctx)
+
+
+class _AverageDown:
+    """average_down's cached tmp MultiFab (the coarsened fine layout, pinned)
+    and its restriction jobs (ghx_avgdown_job: 20 int64 words each)."""
+
+    def __init__(self, fine, coarse, ratio):
+        rix, rmesh, rconfig = (_ref_module(fine, m) for m in ("index_space", "mesh", "config"))
+        self.coarse = weakref.ref(coarse)
+        arena = fine.arena if isinstance(fine.arena, PinnedArena) else PinnedArena()
+        self.tmp = rmesh.MultiFab(rmesh.BoxArray([rix.coarsen(b, ratio) for b in fine.ba]), fine.dm, fine.ncomp, 0,
+                                  arena=arena)
+        d = len(fine.ngrow)
+        fg = tuple(int(v) for v in fine.ngrow) + (0,) * (3 - d)
+        rows = []
+        for gi in fine.local_indices:
+            cb = self.tmp.ba[gi]
+            rows.append([fine.fabs[gi].data.__array_interface__["data"][0], *_rows([fine.ba[gi]], grow=fg)[0],
+                         self.tmp.fabs[gi].data.__array_interface__["data"][0], *_rows([cb])[0], *_rows([cb])[0]])
+        self.jobs = np.ascontiguousarray(np.asarray(rows, np.int64).reshape(-1, 20))
+        self.ratio = np.array([int(ratio)] * d + [1] * (3 - d), np.int32)
+        self.dim, self.ncomp = d, fine.ncomp
+        self.item = next(iter(fine.fabs.values())).data.dtype.itemsize if fine.fabs else 8
+        assert rconfig.spacedim == d
+
+    def run(self) -> None:
+        if len(self.jobs):
+            L = lib()
+            _check(L.ghx_average_down(P(self.jobs.ctypes.data), len(self.jobs), self.ncomp, _p32(self.ratio),
+                                      self.dim, self.item, None))
+            _check(L.ghx_stream_sync(None))
+
+
+def average_down_native(fine, coarse, ratio: int) -> None:
+    """Drop-in body for the reference's amr.average_down (amr.py:235-266):
+    the restriction of every local fine fab into a tmp MultiFab on the
+    coarsened fine layout (one launch), then parallel_copy_native(coarse,
+    tmp); the tmp MultiFab and the jobs are kept per (fine, coarse) pair.
+    Collective under ``runtime_spawn`` (SPMD)."""
+    ratio = int(ratio)
+    if ratio < 1:
+        raise ValueError("ratio must be >= 1")
+    for b in fine.ba:
+        if any(e % ratio for e in b.extents) or any(v % ratio for v in b.lo):
+            raise ValueError(f"fine box {b} is not aligned to ratio {ratio}")
+    if fine.ncomp != coarse.ncomp:
+        raise ValueError("component count mismatch")
+    key = ("ghostx_ad", id(coarse), ratio)
+    prep = fine.plan_cache.get(key)
+    if prep is None or prep.coarse() is not coarse:
+        prep = fine.plan_cache[key] = _AverageDown(fine, coarse, ratio)
+    prep.run()
+    parallel_copy_native(coarse, prep.tmp)
 
 
 def interp_box_native(coarse_fab, fine_fab, fine_region, ratio: int, scheme: str = "pc") -> None:

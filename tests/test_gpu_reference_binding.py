@@ -194,3 +194,80 @@ def test_parallel_copy_rank_threads_through_c_abi_equal_reference(ref, nranks, n
     for r in range(nranks):
         for i in got[r]:
             assert np.array_equal(got[r][i].view(np.uint64), exp[r][i].view(np.uint64)), f"rank {r} fab {i}"
+
+
+def _levels(ix, mesh, n, b, patch_lo, patch_hi, ratio):
+    dom = ix.Box((0, 0, 0), (n - 1,) * 3)
+    cgeom = ix.Geometry(dom, (0.0,) * 3, (1.0,) * 3, (True, True, True))
+    fgeom = cgeom.refined(ratio)
+    cba = mesh.decompose(dom, b)
+    fba = mesh.decompose(ix.Box((patch_lo * ratio,) * 3, ((patch_hi + 1) * ratio - 1,) * 3), b)
+    return cgeom, fgeom, cba, fba
+
+
+@pytest.mark.parametrize("nranks", [1, 2, 3])
+@pytest.mark.parametrize("scheme", ["linear", "piecewise_constant"])
+@pytest.mark.parametrize("patch", [(8, 23), (0, 11)])  # centred patch / patch on the periodic boundary
+def test_fill_patch_through_c_abi_equals_reference(ref, nranks, scheme, patch):
+    _, amr, comm, config, ix, mesh = ref
+    from integration.reference_binding import PinnedArena, fill_patch_native
+    config.set_spacedim(3)
+    cgeom, fgeom, cba, fba = _levels(ix, mesh, 32, 8, patch[0], patch[1], 2)
+
+    def run(native):
+        def program(ctx):
+            arena = PinnedArena() if native else None
+            crse = mesh.MultiFab(cba, mesh.DistributionMapping.round_robin(len(cba), nranks), 2, 0, cgeom,
+                                 arena=arena)
+            fine = mesh.MultiFab(fba, mesh.DistributionMapping.round_robin(len(fba), nranks), 2, 2, fgeom,
+                                 arena=arena)
+            _fill_by_fab(crse, 21)
+            _fill_by_fab(fine, 22)
+            for _ in range(2):
+                if native:
+                    fill_patch_native(fine, crse, fgeom, cgeom, 2, scheme)
+                else:
+                    amr.fill_patch(fine, crse, fgeom, cgeom, 2, scheme, backend=ref[0]._serial)
+            return {i: fine.fabs[i].data.copy() for i in fine.local_indices}, fine.plan_builds
+        return _spawn(comm, nranks, program)
+
+    got, got_stats = run(True)
+    exp, exp_stats = run(False)
+    assert got_stats == exp_stats
+    for r in range(nranks):
+        (g, gb), (e, eb) = got[r], exp[r]
+        assert gb == eb  # plan builds counted like the reference (FillBoundary + fill_patch plans)
+        for i in g:
+            assert np.array_equal(g[i].view(np.uint64), e[i].view(np.uint64)), f"rank {r} fab {i}"
+
+
+@pytest.mark.parametrize("nranks", [1, 2])
+def test_average_down_through_c_abi_equals_reference(ref, nranks):
+    _, amr, comm, config, ix, mesh = ref
+    from integration.reference_binding import PinnedArena, average_down_native
+    config.set_spacedim(3)
+    cgeom, fgeom, cba, fba = _levels(ix, mesh, 32, 8, 4, 19, 2)
+
+    def run(native):
+        def program(ctx):
+            arena = PinnedArena() if native else None
+            crse = mesh.MultiFab(cba, mesh.DistributionMapping.round_robin(len(cba), nranks), 3, 1, cgeom,
+                                 arena=arena)
+            fine = mesh.MultiFab(fba, mesh.DistributionMapping.round_robin(len(fba), nranks), 3, 2, fgeom,
+                                 arena=arena)
+            _fill_by_fab(crse, 31)
+            _fill_by_fab(fine, 32)
+            for _ in range(2):
+                if native:
+                    average_down_native(fine, crse, 2)
+                else:
+                    amr.average_down(fine, crse, 2, backend=ref[0]._serial)
+            return {i: crse.fabs[i].data.copy() for i in crse.local_indices}
+        return _spawn(comm, nranks, program)
+
+    got, got_stats = run(True)
+    exp, exp_stats = run(False)
+    assert got_stats == exp_stats
+    for r in range(nranks):
+        for i in got[r]:
+            assert np.array_equal(got[r][i].view(np.uint64), exp[r][i].view(np.uint64)), f"rank {r} fab {i}"

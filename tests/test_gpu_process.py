@@ -123,9 +123,10 @@ def test_two_processes_one_gpu(cfg):
 # every peer it pushes to; message accounting against the reference's plan
 @pytest.mark.parametrize("world,env", [(4, {}), (4, {"GHX_TRANSPORT": "nccl"}), (8, {}),
                                        (4, {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "30"}),
-                                       (4, {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "30", "GHX_REMOTE": "direct"})],
+                                       (4, {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "30", "GHX_REMOTE": "direct"}),
+                                       (8, {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "60"})],
                          ids=["C3x4-ipc-packed", "C3x4-fallback", "C3x8-ipc-packed", "C3x4-devbarrier",
-                              "C3x4-devsync-direct"])
+                              "C3x4-devsync-direct", "C3x8-devsync"])
 def test_many_processes_one_gpu(world, env):
     _run(("C3", 512, 128, 8, 2, f"C3_x{world}", env), world)
 

@@ -61,6 +61,14 @@ extern "C" {
  * its own host fabs. */
 #define GHX_EXEC_PUSH_PACKED_ALL 6
 #define GHX_EXEC_UNPACK_PACKED_ALL 7
+/* GHX_EXEC_PUSH_PACKED and GHX_EXEC_UNPACK_PACKED of one rank in ONE task
+ * list and one launch (in-kernel synchronisation only, ghx_exec_run_synced):
+ * the pushes first, then the local tags, then the unpacks of the receive
+ * slabs; each peer's DONE is released as soon as this rank's pushes to it
+ * are done, so the slabs that land early are unpacked while later pushes
+ * are still in flight.  Send sizes: ghx_exec_buffer_elems; receive sizes:
+ * ghx_exec_recv_elems. */
+#define GHX_EXEC_EXCHANGE_PACKED 8
 /* OR into the kind of a DIRECT / LOCAL FillBoundary executor whose tags are
  * all local: run the exchange in three phases (x faces; y faces extended over
  * the x ghosts; z faces extended over the x and y ghosts, reading the source
@@ -192,6 +200,11 @@ int ghx_exec_phases(const ghx_exec *ex, int64_t out[4]);
  * 32-byte sector, read from the same fab, so no partial-sector writes;
  * GHX_SECTOR_FILL=0 at create time turns it off). */
 int ghx_exec_sector_fills(const ghx_exec *ex, int64_t *ntags);
+
+/* Per-peer receive-buffer elements of a GHX_EXEC_EXCHANGE_PACKED executor
+ * (what each peer packs for this rank); other kinds: the unpack kinds'
+ * buffer sizes, zeros for the rest.  per_peer: nranks entries. */
+int ghx_exec_recv_elems(const ghx_exec *ex, int64_t *per_peer);
 
 /* Launch-time tuning knob (warps per block * blocks): 0 = default. */
 int ghx_exec_set_grid(ghx_exec *ex, int32_t blocks, int32_t threads);

@@ -21,6 +21,7 @@ EXEC_DIRECT, EXEC_LOCAL, EXEC_PACK, EXEC_UNPACK, EXEC_PUSH_PACKED, EXEC_UNPACK_P
 EXEC_PHASED = 0x100  # flag OR-ed into the kind (include/ghostx.h)
 EXEC_ONLY_XFACES, EXEC_NO_XFACES = 0x200, 0x400  # diagnostic direction split
 EXEC_PUSH_PACKED_ALL, EXEC_UNPACK_PACKED_ALL = 6, 7
+EXEC_EXCHANGE_PACKED = 8
 
 P = C.c_void_p
 I32 = C.c_int32
@@ -62,6 +63,7 @@ _SIGS = {
     "ghx_exec_set_sync": (C.c_int, [P, C.POINTER(P), I32, I32]),
     "ghx_exec_phases": (C.c_int, [P, PI64]),
     "ghx_exec_sector_fills": (C.c_int, [P, PI64]),
+    "ghx_exec_recv_elems": (C.c_int, [P, PI64]),
     "ghx_exec_run_synced": (C.c_int, [P, I64, C.c_uint64, P]),
     "ghx_exec_sync_wait": (C.c_int, [P, C.c_uint64, P]),
     "ghx_arena_create": (C.c_int, [I32, I32, I32, C.c_size_t, C.POINTER(P)]),

@@ -503,6 +503,9 @@ class Executor:
         be = np.zeros(self.nranks, np.int64)
         N.check(N.lib.ghx_exec_buffer_elems(h, N.i64p(be)))
         self.buffer_elems = be
+        re_ = np.zeros(self.nranks, np.int64)
+        N.check(N.lib.ghx_exec_recv_elems(h, N.i64p(re_)))
+        self.recv_elems = re_
         det = np.zeros(8, np.int64)
         N.check(N.lib.ghx_exec_detail(h, N.i64p(det)))
         self.detail = dict(zip(("tags", "tasks", "elems", "alg_bytes", "mirror_tags", "swap_tags", "blocks",
@@ -910,6 +913,7 @@ class Exchange:
             self.sync = "host" if self.mode == "thread" else "none"
         self.remote = "direct"
         self.unp = None
+        self.one_kernel = False
         if self.transport == "nccl":
             self._init_nccl()
         elif self.mode == "process" and host:
@@ -998,12 +1002,25 @@ class Exchange:
         tags, are stored directly into the fabs."""
         plan, src_mf, dst_mf, ctx, me = self.plan, self.src, self.dst, self.ctx, self.ctx.rank
         a = (self.scomp, self.dcomp, self.ncomp)
-        kp, ku = ((N.EXEC_PUSH_PACKED_ALL, N.EXEC_UNPACK_PACKED_ALL) if all_remote
-                  else (N.EXEC_PUSH_PACKED, N.EXEC_UNPACK_PACKED))
-        self.ex = plan.executor(me, kp, src_mf, dst_mf, *a)
-        self.unp = plan.executor(me, ku, src_mf, dst_mf, *a)
+        # with the in-kernel device sync, pushes and unpacks run as ONE
+        # executor and launch (GHX_EXEC_EXCHANGE_PACKED): each peer's DONE is
+        # released when this rank's pushes to it are done, and the slabs that
+        # land early are unpacked while later pushes are in flight
+        # (GHX_ONE_KERNEL=0: push kernel, then unpack kernel)
+        self.one_kernel = (not all_remote and self.sync == "device" and plan.nranks <= 32
+                           and os.environ.get("GHX_FUSED_SYNC", "1") != "0"
+                           and os.environ.get("GHX_ONE_KERNEL", "1") != "0")
+        if self.one_kernel:
+            self.ex = plan.executor(me, N.EXEC_EXCHANGE_PACKED, src_mf, dst_mf, *a)
+            self.unp = None
+            recv_el = self.ex.recv_elems
+        else:
+            kp, ku = ((N.EXEC_PUSH_PACKED_ALL, N.EXEC_UNPACK_PACKED_ALL) if all_remote
+                      else (N.EXEC_PUSH_PACKED, N.EXEC_UNPACK_PACKED))
+            self.ex = plan.executor(me, kp, src_mf, dst_mf, *a)
+            self.unp = plan.executor(me, ku, src_mf, dst_mf, *a)
+            recv_el = self.unp.buffer_elems
         item, n = self.item, plan.nranks
-        recv_el = self.unp.buffer_elems
         offs, total = [], 0
         for r in range(n):
             offs.append(total)
@@ -1029,7 +1046,8 @@ class Exchange:
         # with every remote tag packed, only this rank's own fabs are addressed
         parts = [(dst_mf.local_indices, dst_mf._ptrs)] if all_remote else _ipc_peers(ctx, dst_mf)
         self.table = _table(self.ex, src_mf, parts, bufs)
-        self.t_unp = _table(self.unp, src_mf, [(dst_mf.local_indices, dst_mf._ptrs)], bufs)
+        if self.unp is not None:
+            self.t_unp = _table(self.unp, src_mf, [(dst_mf.local_indices, dst_mf._ptrs)], bufs)
         weakref.finalize(self, _close_ipc, list(self._opened))
         if self.sync == "device":
             self.psync = _process_sync(ctx)
@@ -1101,7 +1119,9 @@ class Exchange:
     # -- launching ---------------------------------------------------------
     @property
     def launches_per_call(self) -> int:
-        return 3 if self.transport == "nccl" else (2 if self.remote in ("packed", "packed_all") else 1)
+        if self.transport == "nccl":
+            return 3
+        return 2 if self.remote in ("packed", "packed_all") and not self.one_kernel else 1
 
     def enqueue(self, stream: int, marks=None) -> None:
         """Put the exchange on ``stream``.  ``marks`` (diagnostics): three
@@ -1121,8 +1141,10 @@ class Exchange:
                 marks[1]()
             if self.unp is not None:
                 self.b_unp.run_synced(stream, e)  # each peer's slab unpacked once its DONE lands
-            else:
+            elif not self.one_kernel:
                 self.ex.sync_wait(e, stream)  # every push into my fabs has landed
+            # (one kernel: its unpack tasks waited for each source's DONE and
+            # its CTA 0 for every peer's before the launch completes)
             if marks:
                 marks[2]()
         elif self.mode == "process" and self.sync == "device":

@@ -645,9 +645,10 @@ struct SyncArgs {
   uint64_t epoch;
   uint64_t timeout_ns;
   int32_t rank, nranks;
-  int32_t mode;             // 0 none, 1 push, 2 unpack / wait
+  int32_t mode;             // 0 none, 1 push, 2 unpack / wait, 3 push + unpack (EXCHANGE_PACKED)
   int32_t nhead;            // mode 1: tasks [0, nhead) are remote
   int32_t pe0, pe1;         // phased executor: tasks [pe0, pe1) phase 1, [pe1, n) phase 2 (0, 0: no phases)
+  const int32_t *peer_total;  // mode 3: push tasks per peer (a peer's DONE when they are all done)
 };
 
 __device__ unsigned int g_sync_timeouts = 0;
@@ -694,13 +695,12 @@ __device__ __forceinline__ void signal_all_peers(const SyncArgs &s, int slot, in
 __global__ void ghx_sync_kernel(const SyncArgs sync) {
   const int lane = threadIdx.x;
   if (lane >= 32) return;
-  if (sync.mode == 1) {
+  if (sync.mode == 1 || sync.mode == 3) {
     __threadfence_system();
     signal_all_peers(sync, kSlotReady, lane);
     signal_all_peers(sync, kSlotDone, lane);
-  } else if (sync.mode == 2) {
-    wait_all_peers(sync, kSlotDone, lane);
   }
+  if (sync.mode == 2 || sync.mode == 3) wait_all_peers(sync, kSlotDone, lane);
 }
 
 // Resolve pointer-table slots into absolute addresses (once per table).
@@ -742,7 +742,11 @@ __global__ void __launch_bounds__(kThreads, RING ? 1 : GHX_MINB) ghx_copy_kernel
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
   }
-  if (sync.mode == 1 && wib == 0) signal_all_peers(sync, kSlotReady, lane);
+  if ((sync.mode == 1 || sync.mode == 3) && wib == 0) signal_all_peers(sync, kSlotReady, lane);
+  if (sync.mode == 3 && blockIdx.x == 0 && wib == 0)
+    for (int p = lane; p < sync.nranks; p += 32)  // peers this rank pushes nothing to: done already
+      if (p != sync.rank && __ldg(sync.peer_total + p) == 0)
+        flag_store(sync.flags[p] + kSlotDone * sync.nranks + sync.rank, sync.epoch);
   uint64_t peers_ok = 0;  // peers whose READY (mode 1) / DONE (mode 2) this warp has seen
   // phased executor: a warp passing into phase p (it grabbed a task of phase
   // p, so it will run no task of an earlier phase again) counts itself in
@@ -795,20 +799,27 @@ __global__ void __launch_bounds__(kThreads, RING ? 1 : GHX_MINB) ghx_copy_kernel
     for (int w = (int)first; w < last; ++w) {
       const int4 nxt = (w + 1 < last) ? __ldg(tasks + w + 1) : tk;
       if (phased) pass_to(w >= sync.pe1 ? 2 : (w >= sync.pe0 ? 1 : 0), true);
-      if ((tk.z >= -1 || tk.z <= kFillTask) && (sync.mode == 2 || (sync.mode == 1 && w < sync.nhead))) {
+      if ((tk.z >= -1 || tk.z <= kFillTask) &&
+          (sync.mode >= 2 || (sync.mode == 1 && w < sync.nhead))) {
         // a remote push waits for the peer's READY, an unpack for its DONE
-        // (both tags of a pair task: they may belong to different peers)
+        // (both tags of a pair task: they may belong to different peers).
+        // Mode 3 tells the two apart by the tag's peer (+ 64: unpack) and
+        // keeps READY peers in bits 0-31 and DONE peers in bits 32-63.
 #pragma unroll 1
         for (int k2 = 0; k2 < 2; ++k2) {
           const int tg = k2 ? (tk.z <= kFillTask ? kFillTask - tk.z : tk.z) : tk.x;
           if (tg < 0) continue;
-          const int peer = __ldg(sync.tag_peer + tg);
-          if (peer >= 0 && peer < 64 && !((peers_ok >> peer) & 1ull)) {
+          const int raw = __ldg(sync.tag_peer + tg);
+          if (raw < 0 || raw >= 128) continue;
+          const bool done_wait = sync.mode == 2 || raw >= 64;
+          const int peer = raw & 63;
+          const int bit = sync.mode == 3 ? (peer & 31) + (done_wait ? 32 : 0) : peer;
+          if (!((peers_ok >> bit) & 1ull)) {
             if (lane == 0)
-              flag_wait(sync.flags[sync.rank] + (sync.mode == 1 ? kSlotReady : kSlotDone) * sync.nranks + peer,
+              flag_wait(sync.flags[sync.rank] + (done_wait ? kSlotDone : kSlotReady) * sync.nranks + peer,
                         sync.epoch, sync.timeout_ns);
             __syncwarp();
-            peers_ok |= 1ull << peer;
+            peers_ok |= 1ull << bit;
           }
         }
       }
@@ -882,19 +893,39 @@ __global__ void __launch_bounds__(kThreads, RING ? 1 : GHX_MINB) ghx_copy_kernel
         store_chunk(ta, (uint32_t)tk.y, lane, va);
         if (tk.z >= 0) store_chunk(tb, (uint32_t)tk.w, lane, vb);
       }
+      if (sync.mode == 3 && w < sync.nhead) {
+        // per-peer DONE: this warp's stores of the task are visible system
+        // wide, then the task is counted against each of its push peers; the
+        // count that completes a peer's total releases the peer's DONE
+        const int4 t0 = __ldg(tasks + w);  // (re-read: a pair task may have swapped roles)
+        __threadfence_system();
+        __syncwarp();
+        if (lane == 0 && t0.z >= -1) {
+          const int pa = __ldg(sync.tag_peer + t0.x);
+          const int pb = t0.z >= 0 ? __ldg(sync.tag_peer + t0.z) : -1;
+#pragma unroll 1
+          for (int k2 = 0; k2 < 2; ++k2) {
+            const int p = k2 ? pb : pa;
+            if (p < 0 || p >= 64 || (k2 && p == pa)) continue;
+            if (atomicAdd(counter + 8 + p, 1ull) + 1 == (unsigned long long)__ldg(sync.peer_total + p))
+              flag_store(sync.flags[p] + kSlotDone * sync.nranks + sync.rank, sync.epoch);
+          }
+        }
+        __syncwarp();
+      }
       tk = nxt;
     }
     nb = __shfl_sync(0xffffffffu, nb, 0);
   }
   if (BULK) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // this lane's bulk stores are done
   if (phased) pass_to(3, false);  // no more tasks: count out of every remaining phase
-  if (sync.mode == 2 && blockIdx.x == 0 && wib == 0) wait_all_peers(sync, kSlotDone, lane);
-  if (sync.mode == 1) __threadfence_system();  // this lane's pushes are visible system-wide
+  if ((sync.mode == 2 || sync.mode == 3) && blockIdx.x == 0 && wib == 0) wait_all_peers(sync, kSlotDone, lane);
+  if (sync.mode == 1 || sync.mode == 3) __threadfence_system();  // this lane's pushes are visible system-wide
   __syncwarp();
   if (lane == 0) {
     const unsigned long long total = (unsigned long long)gridDim.x * (blockDim.x >> 5);
     if (atomicAdd(counter + 1, 1ull) == total - 1) {
-      if (sync.mode == 1) {  // every warp has fenced its pushes: tell the peers
+      if (sync.mode == 1 || sync.mode == 3) {  // every warp has fenced its pushes: tell the peers
         __threadfence_system();
         for (int p = 0; p < sync.nranks; ++p)
           if (p != sync.rank) flag_store(sync.flags[p] + kSlotDone * sync.nranks + sync.rank, sync.epoch);
@@ -904,6 +935,8 @@ __global__ void __launch_bounds__(kThreads, RING ? 1 : GHX_MINB) ghx_copy_kernel
       counter[2] = 0;
       counter[3] = 0;
       counter[4] = 0;
+      if (sync.mode == 3)
+        for (int p = 0; p < sync.nranks; ++p) counter[8 + p] = 0;
     }
   }
 }
@@ -959,6 +992,7 @@ struct HostTag {
   int32_t peer;            // push: destination rank of a remote tag; unpack: source rank; else -1
   int32_t sfab, dfab;      // plan fab ids (pairing)
   int64_t shift[3];
+  bool unpack_role = false;  // reads a receive buffer (unpack kinds, EXCHANGE_PACKED's unpacks)
   // sector fill (unpack of x-face ghosts): the destination's valid x range
   // and the tag's first x, in elements from the storage box's lo (fill_vhi <
   // fill_vlo: not eligible)
@@ -1119,6 +1153,7 @@ struct ghx_exec {
   int64_t nring = 0;
   std::vector<uint8_t> swap_fab;  // fabs touched by sector-swap tasks
   std::vector<int64_t> buf_elems;  // per peer (pack: send, unpack: recv)
+  std::vector<int64_t> recv_elems; // per peer, receive side (EXCHANGE_PACKED; unpack kinds = buf_elems)
   std::vector<DevTag> htags;
   std::vector<PairKey> hkeys;
   std::vector<int32_t> hremote;
@@ -1137,6 +1172,13 @@ struct ghx_exec {
   int32_t sync_rank = -1, sync_n = 0;
   uint64_t **dflags = nullptr;
   int32_t *dpeer = nullptr;
+  int32_t rank = 0;  // the rank this executor was compiled for
+  // EXCHANGE_PACKED: remote push tasks per destination peer (a pair task
+  // counted once per distinct peer); the kernel releases a peer's DONE when
+  // its last push task to that peer is done
+  std::vector<int32_t> peer_total;
+  int32_t *dpeer_total = nullptr;
+  int32_t nunpack = 0;  // EXCHANGE_PACKED: unpack tasks at the tail of htasks
   std::vector<int4> htasks;
   std::vector<int> hchain;  // chain tables (tag indices of consecutive seams)
   int *dchain = nullptr;
@@ -1198,8 +1240,12 @@ void add_devtag(ghx_exec *ex, const HostTag &t, int64_t x0, int64_t nxe, int vl,
   g.vlog = (uint8_t)vl;
   ex->htags.push_back(g);
   ex->hkeys.emplace_back(t.sfab, t.dfab, t.shift[0], t.shift[1], t.shift[2], part, g.nxv, g.ny, g.nz, vl);
-  ex->hremote.push_back(t.remote ? 1 : 0);
-  ex->hpeer.push_back(t.peer);
+  // hremote: 1 remote, 2 the unpack side of an EXCHANGE_PACKED executor;
+  // hpeer: the peer, + 64 for that unpack side (the kernel waits for the
+  // peer's DONE instead of its READY)
+  const bool xunpack = ex->kind == GHX_EXEC_EXCHANGE_PACKED && t.unpack_role;
+  ex->hremote.push_back(xunpack ? 2 : (t.remote ? 1 : 0));
+  ex->hpeer.push_back(xunpack ? t.peer + 64 : t.peer);
   ex->hphase.push_back(ex->cur_phase);
   // sector fill: one 16-byte vector per row, every row in the same sector
   // half (even strides), and the other half of its sectors valid cells
@@ -1332,14 +1378,15 @@ void build_tasks(ghx_exec *ex) {
     return !v || std::atoi(v) != 0;
   }();
   if (pair_remote) {
-    const bool unpack = ex->kind == GHX_EXEC_UNPACK || ex->kind == GHX_EXEC_UNPACK_PACKED ||
-                        ex->kind == GHX_EXEC_UNPACK_PACKED_ALL;
-    std::map<std::tuple<int32_t, uint32_t, uint32_t, uint32_t, uint32_t, int>, int32_t> open;
+    const bool unpack_kind = ex->kind == GHX_EXEC_UNPACK || ex->kind == GHX_EXEC_UNPACK_PACKED ||
+                             ex->kind == GHX_EXEC_UNPACK_PACKED_ALL;
+    std::map<std::tuple<int32_t, uint32_t, uint32_t, uint32_t, uint32_t, int, int>, int32_t> open;
     for (size_t i = 0; i < n; ++i) {
       if (mate[i] >= 0 || !ex->hremote[i]) continue;
       const DevTag &t = ex->htags[i];
+      const bool unpack = unpack_kind || ex->hremote[i] == 2;
       const auto key = std::make_tuple(unpack ? std::get<1>(ex->hkeys[i]) : std::get<0>(ex->hkeys[i]), t.nxv, t.ny,
-                                       t.nz, t.nvec, (int)t.vlog);
+                                       t.nz, t.nvec, (int)t.vlog, (int)ex->hremote[i]);
       auto it = open.find(key);
       if (it == open.end()) {
         open.emplace(key, (int32_t)i);
@@ -1350,7 +1397,7 @@ void build_tasks(ghx_exec *ex) {
       }
     }
   }
-  std::vector<int4> loc, rem, swaps;
+  std::vector<int4> loc, rem, swaps, unp;  // unp: EXCHANGE_PACKED's unpack tasks
   ex->npaired = 0;
   ex->nswap = 0;
   ex->nring = 0;
@@ -1379,7 +1426,7 @@ void build_tasks(ghx_exec *ex) {
   };
   for (size_t i = 0; i < n; ++i) {
     const uint32_t nv = ex->htags[i].nvec;
-    auto &out = ex->hremote[i] ? rem : loc;
+    auto &out = ex->hremote[i] == 2 ? unp : (ex->hremote[i] ? rem : loc);
     if (mate[i] >= 0) {
       if ((size_t)mate[i] < i) continue;
       const int lo = allow_swap ? swap_low(ex, (int)i, mate[i]) : -1;
@@ -1531,6 +1578,30 @@ void build_tasks(ghx_exec *ex) {
     const char *v = std::getenv("GHX_REMOTE_ORDER");
     return v && std::string(v) == "interleave";
   }();
+  // EXCHANGE_PACKED: pushes in peer-distance order (rank r serves r+1
+  // first, then r+2, ...: every peer's DONE is released in turn, and at any
+  // moment the ranks push to different peers), unpacks in arrival order
+  // (r-1's slab first, then r-2's, ...)
+  if (ex->kind == GHX_EXEC_EXCHANGE_PACKED) {
+    const int n = std::max(1, ex->nranks);
+    auto order = [&](std::vector<int4> &v, bool arrival) {
+      auto dist = [&](int32_t tag) -> int {
+        if (tag < 0 || ex->hpeer[tag] < 0) return n;
+        const int p = ex->hpeer[tag] & 63;
+        return arrival ? (ex->rank - p + n) % n : (p - ex->rank + n) % n;
+      };
+      auto key = [&](const int4 &t) { return std::min(dist(t.x), dist(t.z >= 0 ? t.z : -1)); };
+      std::stable_sort(v.begin(), v.end(), [&](const int4 &l, const int4 &r) { return key(l) < key(r); });
+    };
+    order(rem, false);
+    order(unp, true);
+  }
+  ex->peer_total.assign(64, 0);
+  for (const int4 &t : rem) {
+    const int32_t pa = ex->hpeer[t.x], pb = t.z >= 0 ? ex->hpeer[t.z] : -1;
+    if (pa >= 0 && pa < 64) ex->peer_total[pa] += 1;
+    if (pb >= 0 && pb < 64 && pb != pa) ex->peer_total[pb] += 1;
+  }
   ex->nhead = 0;
   if (!b.empty() && !interleave) {
     std::vector<int4> merged(b);
@@ -1580,6 +1651,10 @@ void build_tasks(ghx_exec *ex) {
     ex->pe0 = c0;
     ex->pe1 = c1;
   }
+  // the unpacks last: every push and local task is grabbed before a warp
+  // can wait on a peer's DONE
+  ex->nunpack = (int32_t)unp.size();
+  a.insert(a.end(), unp.begin(), unp.end());
   ex->htasks.swap(a);
 }
 
@@ -1606,7 +1681,7 @@ int ghx_exec_create(const ghx_plan *plan, int32_t rank, int32_t kind, const int6
   const int xsel = kind & (GHX_EXEC_ONLY_XFACES | GHX_EXEC_NO_XFACES | 0x800);
   kind &= ~(GHX_EXEC_PHASED | GHX_EXEC_ONLY_XFACES | GHX_EXEC_NO_XFACES | 0x800);
   if (!plan || !out || (plan->nsrc && !src_fab_boxes) || (plan->ndst && !dst_fab_boxes) ||
-      rank < 0 || rank >= plan->nranks || kind < GHX_EXEC_DIRECT || kind > GHX_EXEC_UNPACK_PACKED_ALL ||
+      rank < 0 || rank >= plan->nranks || kind < GHX_EXEC_DIRECT || kind > GHX_EXEC_EXCHANGE_PACKED ||
       (elem_bytes != 4 && elem_bytes != 8) || ncomp < 1 || scomp < 0 || dcomp < 0 ||
       scomp + ncomp > src_ncomp_total || dcomp + ncomp > dst_ncomp_total) {
     set_error("ghx_exec_create: bad arguments");
@@ -1621,6 +1696,7 @@ int ghx_exec_create(const ghx_plan *plan, int32_t rank, int32_t kind, const int6
   }
   ex->device = device;
   ex->kind = kind;
+  ex->rank = rank;
   ex->nranks = plan->nranks;
   ex->nsrc = plan->nsrc;
   ex->ndst = plan->ndst;
@@ -1642,6 +1718,7 @@ int ghx_exec_create(const ghx_plan *plan, int32_t rank, int32_t kind, const int6
   const int32_t send_base = plan->nsrc + plan->ndst;
   const int32_t recv_base = send_base + plan->nranks;
   std::vector<int64_t> buf_off(plan->nranks, 0);
+  std::vector<int64_t> recv_off(plan->nranks, 0);  // EXCHANGE_PACKED: the unpack side's receive slabs
   // remote tags with narrow rows travel packed (contiguous over NVLink);
   // the rule is identical on every rank, so pushes and unpacks agree
   static const int64_t pack_row_bytes = [] {
@@ -1673,6 +1750,15 @@ int ghx_exec_create(const ghx_plan *plan, int32_t rank, int32_t kind, const int6
       case GHX_EXEC_PUSH_PACKED_ALL: take = p.srank == rank; dst_is_fab = !packable(p); break;
       case GHX_EXEC_UNPACK_PACKED:
       case GHX_EXEC_UNPACK_PACKED_ALL: take = p.drank == rank && packable(p); src_is_fab = false; break;
+      case GHX_EXEC_EXCHANGE_PACKED:  // this rank's pushes (as PUSH_PACKED) and unpacks (as UNPACK_PACKED)
+        if (p.srank == rank) {
+          take = true;
+          dst_is_fab = !packable(p);
+        } else if (p.drank == rank && packable(p)) {
+          take = true;
+          src_is_fab = false;
+        }
+        break;
     }
     if (take && xsel && plan->mode == GHX_MODE_FILL_BOUNDARY && (int64_t)plan->vbox.size() == plan->ndst) {
       // diagnostic split: x-face tags (outside the valid box in x only) or the rest
@@ -1737,12 +1823,14 @@ int ghx_exec_create(const ghx_plan *plan, int32_t rank, int32_t kind, const int6
       t.s.sc = S.nx * S.ny * S.nz;
       t.s.ptr = p.src;
     } else {  // unpack: dense F-order piece inside the recv buffer from srank
-      t.s.off = buf_off[p.srank];
+      std::vector<int64_t> &off = kind == GHX_EXEC_EXCHANGE_PACKED ? recv_off : buf_off;
+      t.s.off = off[p.srank];
       t.s.sy = t.nx;
       t.s.sz = t.nx * t.ny;
       t.s.sc = cells;
       t.s.ptr = recv_base + p.srank;
-      buf_off[p.srank] += cells * ncomp;
+      off[p.srank] += cells * ncomp;
+      t.unpack_role = true;
     }
     if (dst_is_fab) {
       t.d.off = (p.dbox.lo[0] - D.box.lo[0]) +
@@ -1788,6 +1876,10 @@ int ghx_exec_create(const ghx_plan *plan, int32_t rank, int32_t kind, const int6
     return GHX_EINVAL;
   }
   ex->buf_elems = buf_off;
+  ex->recv_elems = kind == GHX_EXEC_EXCHANGE_PACKED ? recv_off
+                   : (kind == GHX_EXEC_UNPACK || kind == GHX_EXEC_UNPACK_PACKED || kind == GHX_EXEC_UNPACK_PACKED_ALL)
+                       ? buf_off
+                       : std::vector<int64_t>(plan->nranks, 0);
   if (ex->htags.size() >= (size_t)INT32_MAX) {
     set_error("ghx_exec_create: too many tags");
     delete ex;
@@ -1885,6 +1977,7 @@ void ghx_exec_free(ghx_exec *ex) {
   if (ex->dptrs) cudaFree(ex->dptrs);
   if (ex->dflags) cudaFree(ex->dflags);
   if (ex->dpeer) cudaFree(ex->dpeer);
+  if (ex->dpeer_total) cudaFree(ex->dpeer_total);
   delete ex;
 }
 
@@ -1992,6 +2085,15 @@ int ghx_exec_phases(const ghx_exec *ex, int64_t out[4]) {
   return GHX_OK;
 }
 
+int ghx_exec_recv_elems(const ghx_exec *ex, int64_t *per_peer) {
+  if (!ex || !per_peer) {
+    set_error("ghx_exec_recv_elems: bad arguments");
+    return GHX_EINVAL;
+  }
+  for (size_t i = 0; i < ex->recv_elems.size(); ++i) per_peer[i] = ex->recv_elems[i];
+  return GHX_OK;
+}
+
 int ghx_exec_sector_fills(const ghx_exec *ex, int64_t *ntags) {
   if (!ex || !ntags) {
     set_error("ghx_exec_sector_fills: bad arguments");
@@ -2061,8 +2163,9 @@ int find_or_bind(ghx_exec *ex, void *const *ptrs, int64_t nptrs, cudaStream_t st
     std::unique_ptr<ghx_exec::Binding> nb(new ghx_exec::Binding());
     cudaError_t e = cudaMalloc(&nb->dtags, std::max<size_t>(1, ex->htags.size()) * sizeof(DevTag));
     if (e == cudaSuccess) e = cudaMalloc(&nb->dptrs, std::max<int64_t>(ex->nptrs, 1) * sizeof(void *));
-    if (e == cudaSuccess) e = cudaMalloc(&nb->counter, 8 * sizeof(unsigned long long));
-    if (e == cudaSuccess) e = cudaMemsetAsync(nb->counter, 0, 8 * sizeof(unsigned long long), st);
+    // [0, 8) scheduler / phase counters, [8, 72) EXCHANGE_PACKED's per-peer push counts
+    if (e == cudaSuccess) e = cudaMalloc(&nb->counter, 72 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemsetAsync(nb->counter, 0, 72 * sizeof(unsigned long long), st);
     if (e == cudaSuccess && !ex->htags.empty())
       e = cudaMemcpyAsync(nb->dtags, ex->dtags, ex->htags.size() * sizeof(DevTag), cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) {
@@ -2249,6 +2352,10 @@ int ghx_exec_set_sync(ghx_exec *ex, uint64_t *const *flag_arrays, int32_t rank, 
     set_error("ghx_exec_set_sync: bad arguments (nranks <= 64, matching the plan)");
     return GHX_EINVAL;
   }
+  if (ex->kind == GHX_EXEC_EXCHANGE_PACKED && nranks > 32) {
+    set_error("ghx_exec_set_sync: GHX_EXEC_EXCHANGE_PACKED synchronises at most 32 ranks");
+    return GHX_EINVAL;
+  }
   for (int i = 0; i < nranks; ++i)
     if (!flag_arrays[i]) {
       set_error("ghx_exec_set_sync: null flag array");
@@ -2263,6 +2370,9 @@ int ghx_exec_set_sync(ghx_exec *ex, uint64_t *const *flag_arrays, int32_t rank, 
     e = cudaMalloc(&ex->dpeer, std::max<size_t>(1, ex->hpeer.size()) * sizeof(int32_t));
   if (e == cudaSuccess && !ex->hpeer.empty())
     e = cudaMemcpy(ex->dpeer, ex->hpeer.data(), ex->hpeer.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && !ex->dpeer_total) e = cudaMalloc(&ex->dpeer_total, 64 * sizeof(int32_t));
+  if (e == cudaSuccess && ex->peer_total.size() == 64)
+    e = cudaMemcpy(ex->dpeer_total, ex->peer_total.data(), 64 * sizeof(int32_t), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return cuda_fail(e, "ghx_exec_set_sync");
   ex->sync_rank = rank;
   ex->sync_n = nranks;
@@ -2283,6 +2393,7 @@ static int sync_args(ghx_exec *ex, uint64_t epoch, int32_t mode, SyncArgs *out) 
   s.nranks = ex->sync_n;
   s.mode = mode;
   s.nhead = ex->nhead;
+  s.peer_total = ex->dpeer_total;
   *out = s;
   return GHX_OK;
 }
@@ -2295,14 +2406,16 @@ int ghx_exec_run_synced(ghx_exec *ex, int64_t binding, uint64_t epoch, void *str
   const bool unpack = ex->kind == GHX_EXEC_UNPACK_PACKED || ex->kind == GHX_EXEC_UNPACK_PACKED_ALL;
   const bool push = ex->kind == GHX_EXEC_DIRECT || ex->kind == GHX_EXEC_PUSH_PACKED ||
                     ex->kind == GHX_EXEC_PUSH_PACKED_ALL;
-  if (!unpack && !push) {
-    set_error("ghx_exec_run_synced: only push (direct / packed) and packed-unpack executors synchronise in-kernel");
+  const bool both = ex->kind == GHX_EXEC_EXCHANGE_PACKED;
+  if (!unpack && !push && !both) {
+    set_error("ghx_exec_run_synced: only push (direct / packed), packed-unpack and exchange executors "
+              "synchronise in-kernel");
     return GHX_EINVAL;
   }
   std::lock_guard<std::mutex> lk(ex->mu);
   DeviceGuard g(ex->device);
   SyncArgs s;
-  if (int rc = sync_args(ex, epoch, unpack ? 2 : 1, &s)) return rc;
+  if (int rc = sync_args(ex, epoch, both ? 3 : (unpack ? 2 : 1), &s)) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (ex->htasks.empty()) {  // nothing to move: still signal (push) / wait (unpack)
     ghx_sync_kernel<<<1, 32, 0, st>>>(s);

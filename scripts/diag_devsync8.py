@@ -1,6 +1,8 @@
-"""Diagnostic: C3 across 8 processes on one GPU with device sync -- the
-serial unpack, the concurrent unpack with end-of-kernel DONE, and the
-concurrent unpack with per-peer DONE (tests/test_gpu_process.py workers)."""
+"""Diagnostic: C3 across N processes (DIAG_WORLD, default 8) on one GPU with
+the in-kernel device sync -- the one-kernel packed exchange (pushes, local
+tags and unpacks in one launch), the push-then-unpack pair, direct remote
+stores -- through tests/test_gpu_process.py's workers; pass variant names
+(repeats allowed) to choose."""
 import os
 import sys
 import time
@@ -9,10 +11,9 @@ sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
 
 VARIANTS = {
-    "serial-unpack": {"GHX_UNPACK_OVERLAP": "0"},
-    "overlap-kernel-done": {"GHX_UNPACK_OVERLAP": "1", "GHX_PEER_DONE": "0"},
-    "overlap-peer-done": {"GHX_UNPACK_OVERLAP": "1"},
-    "serial-unpack-peer-done": {"GHX_UNPACK_OVERLAP": "0", "GHX_PEER_DONE": "1"},
+    "one-kernel": {},
+    "two-kernels": {"GHX_ONE_KERNEL": "0"},
+    "direct": {"GHX_REMOTE": "direct"},
 }
 
 if __name__ == "__main__":

@@ -204,3 +204,37 @@ def test_unpack_x_ghosts_run_as_sector_fills(monkeypatch):
     assert sector_fills(64, 16, 2, 2, N.EXEC_UNPACK_PACKED, item=4) == 0
     # f32 ng 4: 16-byte rows again
     assert sector_fills(64, 16, 2, 4, N.EXEC_UNPACK_PACKED, item=4) == 32 * 2
+
+
+def test_exchange_packed_combines_push_and_unpack():
+    """GHX_EXEC_EXCHANGE_PACKED = PUSH_PACKED + UNPACK_PACKED of one rank in
+    one task list: same tags, same send / receive buffer sizes."""
+    boxes = gu.scale_boxes(64, 16)
+    ranks = [i % 4 for i in range(len(boxes))]
+    h = native_fb(boxes, [2] * 3, [1, 1, 1], [64] * 3, ranks, 4)
+    storage = boxes.copy()
+    storage[:, :3] -= 2
+    storage[:, 3:] += 2
+    storage = np.ascontiguousarray(storage)
+
+    def info(kind):
+        ex = C.c_void_p()
+        N.check(N.lib.ghx_exec_create(h, 1, kind, N.i64p(storage), 2, N.i64p(storage), 2, 0, 0, 2, 8, 0,
+                                      C.byref(ex)))
+        try:
+            a = [C.c_int64() for _ in range(4)]
+            N.check(N.lib.ghx_exec_info(ex, *[C.byref(v) for v in a]))
+            send, recv = np.zeros(4, np.int64), np.zeros(4, np.int64)
+            N.check(N.lib.ghx_exec_buffer_elems(ex, N.i64p(send)))
+            N.check(N.lib.ghx_exec_recv_elems(ex, N.i64p(recv)))
+            return a[0].value, a[2].value, send, recv
+        finally:
+            N.lib.ghx_exec_free(ex)
+    try:
+        tp, ep, sp, _ = info(N.EXEC_PUSH_PACKED)
+        tu, eu, _, ru = info(N.EXEC_UNPACK_PACKED)
+        tx, ex_, sx, rx = info(N.EXEC_EXCHANGE_PACKED)
+        assert tx == tp + tu and ex_ == ep + eu
+        assert np.array_equal(sx, sp) and np.array_equal(rx, ru) and rx.sum() > 0
+    finally:
+        N.lib.ghx_plan_free(h)

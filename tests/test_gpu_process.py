@@ -124,9 +124,10 @@ def test_two_processes_one_gpu(cfg):
 @pytest.mark.parametrize("world,env", [(4, {}), (4, {"GHX_TRANSPORT": "nccl"}), (8, {}),
                                        (4, {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "30"}),
                                        (4, {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "30", "GHX_REMOTE": "direct"}),
-                                       (8, {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "60"})],
+                                       (8, {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "60"}),
+                                       (8, {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "60", "GHX_ONE_KERNEL": "0"})],
                          ids=["C3x4-ipc-packed", "C3x4-fallback", "C3x8-ipc-packed", "C3x4-devbarrier",
-                              "C3x4-devsync-direct", "C3x8-devsync"])
+                              "C3x4-devsync-direct", "C3x8-devsync", "C3x8-devsync-two-kernels"])
 def test_many_processes_one_gpu(world, env):
     _run(("C3", 512, 128, 8, 2, f"C3_x{world}", env), world)
 

@@ -81,8 +81,9 @@ def _worker(rank, port, q, names, env):
 
 @pytest.mark.parametrize("env", [{}, {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "20"},
                                  {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "20", "GHX_REMOTE": "direct"},
-                                 {"GHX_TRANSPORT": "nccl"}],
-                         ids=["host-sync-packed", "devsync-packed", "devsync-direct", "fallback"])
+                                 {"GHX_TRANSPORT": "nccl"},
+                                 {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "20", "GHX_ONE_KERNEL": "0"}],
+                         ids=["host-sync-packed", "devsync-packed", "devsync-direct", "fallback", "devsync-two-kernels"])
 def test_two_process_golden_fill_boundary(env):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()

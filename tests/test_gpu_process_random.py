@@ -92,8 +92,10 @@ def _worker(rank, world, port, q, seed0, env):
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("env", [{}, {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "20"},
                                  {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "20", "GHX_REMOTE": "direct"},
-                                 {"GHX_TRANSPORT": "nccl"}, {"GHX_SECTOR_FILL": "0"}],
-                         ids=["host-sync-packed", "devsync-packed", "devsync-direct", "fallback", "no-sector-fill"])
+                                 {"GHX_TRANSPORT": "nccl"}, {"GHX_SECTOR_FILL": "0"},
+                                 {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "20", "GHX_ONE_KERNEL": "0"}],
+                         ids=["host-sync-packed", "devsync-packed", "devsync-direct", "fallback", "no-sector-fill",
+                              "devsync-two-kernels"])
 def test_random_layouts_across_processes(world, env):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()

@@ -2,7 +2,8 @@
 # Multi-GPU measurement pass for a box with N >= 2 B200s (one process per
 # GPU, NCCL plumbing): the north-star C3 first (BASELINE configs[2], the
 # bench default), then C5 and C2, at 2/4/8 GPUs over the CUDA-IPC push
-# (packed and direct remote rows; in-kernel READY/DONE sync, plus the
+# (packed remote rows in one push + unpack launch, the same as two launches
+# GHX_ONE_KERNEL=0, direct remote rows; in-kernel READY/DONE sync, plus the
 # standalone-barrier sequence GHX_FUSED_SYNC=0 for comparison) and the NCCL
 # pack/send/unpack fallback.
 # Output: gpurun_out/multi/<config>_<transport>_<N>.json (one bench line each).
@@ -17,7 +18,8 @@ for cfg in C3 C5 C2; do
   steps=100; [ "$cfg" = C5 ] && steps=20
   for n in 2 4 8; do
     [ "$n" -le "$MAXG" ] || continue
-    for variant in "p2p:GHX_REMOTE=packed" "p2p:GHX_REMOTE=direct" "p2pbar:GHX_FUSED_SYNC=0" "nccl:GHX_TRANSPORT=nccl"; do
+    for variant in "p2p:GHX_REMOTE=packed" "p2p2k:GHX_ONE_KERNEL=0" "p2p:GHX_REMOTE=direct" "p2pbar:GHX_FUSED_SYNC=0" \
+                   "nccl:GHX_TRANSPORT=nccl"; do
       tag=${variant%%:*}; envs=${variant#*:}
       port=$((port + 1))
       env $envs GHX_BARRIER_TIMEOUT_S=30 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n \

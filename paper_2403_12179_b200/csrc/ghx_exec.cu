@@ -1403,7 +1403,12 @@ void build_tasks(ghx_exec *ex) {
   ex->nring = 0;
   ex->hchain.clear();
   ex->swap_fab.clear();
-  const bool allow_swap = std::getenv("GHX_NO_SWAP") == nullptr;
+  // an EXCHANGE_PACKED executor with sector fills runs in the fill-capable
+  // kernel instantiation, which carries no sector-swap / chain tasks (their
+  // registers): its local mirror pairs run as pair copies instead
+  bool any_fill = false;
+  for (size_t i = 0; i < n && !ex->ring; ++i) any_fill = any_fill || (i < ex->hfill.size() && ex->hfill[i]);
+  const bool allow_swap = std::getenv("GHX_NO_SWAP") == nullptr && !(ex->kind == GHX_EXEC_EXCHANGE_PACKED && any_fill);
   std::vector<int32_t> swap_lo;  // low tag of every sector-swap pair
   ex->nbulk = 0;
   auto bulk_ok = [&](size_t i) {
@@ -1731,7 +1736,8 @@ int ghx_exec_create(const ghx_plan *plan, int32_t rank, int32_t kind, const int6
   };
   // sector fill for the unpack kinds of a FillBoundary (GHX_SECTOR_FILL=0: off)
   const char *sf = std::getenv("GHX_SECTOR_FILL");
-  const bool fill_ok = (kind == GHX_EXEC_UNPACK || kind == GHX_EXEC_UNPACK_PACKED || kind == GHX_EXEC_UNPACK_PACKED_ALL) &&
+  const bool fill_ok = (kind == GHX_EXEC_UNPACK || kind == GHX_EXEC_UNPACK_PACKED || kind == GHX_EXEC_UNPACK_PACKED_ALL ||
+                        kind == GHX_EXEC_EXCHANGE_PACKED) &&
                        plan->mode == GHX_MODE_FILL_BOUNDARY && !plan->clipped &&
                        (int64_t)plan->vbox.size() == plan->ndst && !(sf && std::atoi(sf) == 0);
   int64_t bad = -1;

@@ -227,6 +227,11 @@ def test_exchange_packed_combines_push_and_unpack():
             send, recv = np.zeros(4, np.int64), np.zeros(4, np.int64)
             N.check(N.lib.ghx_exec_buffer_elems(ex, N.i64p(send)))
             N.check(N.lib.ghx_exec_recv_elems(ex, N.i64p(recv)))
+            fills, kinds = C.c_int64(), np.zeros(6, np.int64)
+            N.check(N.lib.ghx_exec_sector_fills(ex, C.byref(fills)))
+            N.check(N.lib.ghx_exec_task_kinds(ex, N.i64p(kinds)))
+            if kind == N.EXEC_EXCHANGE_PACKED:  # fills ride in the instantiation without swap / chain tasks
+                assert fills.value > 0 and kinds[1] == 0 and kinds[2] == 0
             return a[0].value, a[2].value, send, recv
         finally:
             N.lib.ghx_exec_free(ex)

@@ -651,7 +651,10 @@ def run_ours(args, cfg, rank, world):
         v = torch.tensor([statistics.median(push), statistics.median(tail)], dtype=torch.float64, device=dev)
         dist.all_reduce(v, op=dist.ReduceOp.MAX)
         breakdown = {"push_kernel_ms": round(float(v[0]), 5), "unpack_or_wait_ms": round(float(v[1]), 5),
-                     "remote": x.remote, "note": "median per rank, max over ranks; push includes the READY waits"}
+                     "remote": x.remote, "one_kernel": bool(getattr(x, "one_kernel", False)),
+                     "note": "median per rank, max over ranks; push includes the READY waits"
+                             + ("; one kernel: push_kernel_ms is the whole exchange (pushes, local tags and "
+                                "unpacks in one launch)" if getattr(x, "one_kernel", False) else "")}
     launches = N.lib.ghx_launch_count() - l0
     if dist:
         dist.barrier()

@@ -559,6 +559,37 @@ __device__ __forceinline__ void tile_ring_task(const DevTag *__restrict__ tags, 
   }
 }
 
+// Seam task (host-memory pack / unpack of one fab's remote x faces, see
+// seam_pair_hi): one column q (z, component) of rows; lane pair p takes seam
+// chunk c = step * 16 + p - 1, side 0 moves H's row c, side 1 L's row c + 1.
+// Pack reads the chunk's two 32-byte halves (adjacent lanes: one 64-byte
+// PCIe read) and stores each side's 16-byte vector into its peer's slab;
+// unpack reads the two slab vectors and stores them to the adjacent ghost
+// halves (one PCIe write).
+template <int LD>
+__device__ __forceinline__ void seam_task(const DevTag &H, const DevTag &L, uint32_t q, bool pack, int lane) {
+  const int p = lane >> 1, side = lane & 1;
+  const int ny = (int)H.ny;
+  const DevTag &T = side ? L : H;
+#pragma unroll 1
+  for (int c0 = -1; c0 < ny; c0 += 16) {
+    const int c = c0 + p;
+    const int row = side ? c + 1 : c;
+    if (c >= ny || row < 0 || row >= ny) continue;
+    const uint32_t v = (uint32_t)row + (uint32_t)ny * q;  // one vector per row
+    const char *src = reinterpret_cast<const char *>(T.src) + (vec_offset<true>(T, v) << 4);
+    char *dst = reinterpret_cast<char *>(T.dst) + (vec_offset<false>(T, v) << 4);
+    uint4 val;
+    if (pack) {  // side 0: [H.src | hg], side 1: [lg | L.src] -- the chunk's two halves
+      const u8x32 h = ld32<LD>(side ? src - 16 : src);
+      val = side ? make_uint4(h.w[4], h.w[5], h.w[6], h.w[7]) : make_uint4(h.w[0], h.w[1], h.w[2], h.w[3]);
+    } else {
+      val = ld16<LD>(src);
+    }
+    *reinterpret_cast<uint4 *>(dst) = val;
+  }
+}
+
 // Bulk-row task (TMA 1-D bulk copies): rows of a 16-byte-vector tag are
 // moved global -> shared -> global by the copy engine of the SM, one lane
 // per row (cp.async.bulk with an mbarrier per warp), so a warp keeps
@@ -799,7 +830,7 @@ __global__ void __launch_bounds__(kThreads, RING ? 1 : GHX_MINB) ghx_copy_kernel
     for (int w = (int)first; w < last; ++w) {
       const int4 nxt = (w + 1 < last) ? __ldg(tasks + w + 1) : tk;
       if (phased) pass_to(w >= sync.pe1 ? 2 : (w >= sync.pe0 ? 1 : 0), true);
-      if ((tk.z >= -1 || tk.z <= kFillTask) &&
+      if ((tk.z >= -1 || tk.z <= kFillTask || tk.z == -7 || tk.z == -8) &&
           (sync.mode >= 2 || (sync.mode == 1 && w < sync.nhead))) {
         // a remote push waits for the peer's READY, an unpack for its DONE
         // (both tags of a pair task: they may belong to different peers).
@@ -807,7 +838,7 @@ __global__ void __launch_bounds__(kThreads, RING ? 1 : GHX_MINB) ghx_copy_kernel
         // keeps READY peers in bits 0-31 and DONE peers in bits 32-63.
 #pragma unroll 1
         for (int k2 = 0; k2 < 2; ++k2) {
-          const int tg = k2 ? (tk.z <= kFillTask ? kFillTask - tk.z : tk.z) : tk.x;
+          const int tg = k2 ? (tk.z <= kFillTask ? kFillTask - tk.z : (tk.z == -7 || tk.z == -8) ? tk.w : tk.z) : tk.x;
           if (tg < 0) continue;
           const int raw = __ldg(sync.tag_peer + tg);
           if (raw < 0 || raw >= 128) continue;
@@ -829,6 +860,16 @@ __global__ void __launch_bounds__(kThreads, RING ? 1 : GHX_MINB) ghx_copy_kernel
         ring_task<LD>(tags, chains, tk.x, tk.w, tk.y, lane);
       } else if (RING && tk.z == -6) {  // tile ring task: k fabs x 16/k consecutive seam chunks per step
         tile_ring_task<LD>(tags, chains, tk.x, tk.y, tk.w, lane);
+      } else if (RING && (tk.z == -7 || tk.z == -8)) {  // seam pack / unpack task: column tk.y of tags tk.x (H), tk.w (L)
+        if (tk.x != have_a || tk.w != have_b) {
+          __syncwarp();
+          if (tk.x != have_a) fetch_tag(tags, tk.x, &ta, lane);
+          if (tk.w != have_b) fetch_tag(tags, tk.w, &tb, lane);
+          have_a = tk.x;
+          have_b = tk.w;
+          __syncwarp();
+        }
+        seam_task<LD>(ta, tb, (uint32_t)tk.y, tk.z == -7, lane);
       } else if (BULK && tk.z == -5) {  // bulk-row task: tk.w rows of tag tk.x from row tk.y
         if (tk.x != have_a || have_b != -5) {
           __syncwarp();
@@ -1167,6 +1208,7 @@ struct ghx_exec {
   std::vector<int8_t> hphase;   // per tag
   std::vector<uint8_t> hfill;   // per tag: 16-byte ghost halves written as whole sectors (fill_load)
   int64_t nfill = 0;            // tags run as sector-fill tasks
+  int64_t nseam = 0;            // tags run as seam pack / unpack tasks (host memory, remote x faces)
   int32_t pe0 = 0, pe1 = 0;
   // in-kernel synchronisation (ghx_exec_set_sync)
   int32_t sync_rank = -1, sync_n = 0;
@@ -1310,6 +1352,33 @@ int swap_low(const ghx_exec *ex, int ia, int ib) {
   return -1;
 }
 
+// Seam pairs of one fab's remote x faces over PCIe (host-memory pack and
+// unpack executors): H moves the high-x 16-byte vector of every row, L the
+// low-x one, of the SAME fab rows.  The end of row y and the start of row
+// y+1 are one 64-byte seam chunk, so a lane pair can move H's row y and
+// L's row y+1 with one coalesced request instead of two 16-byte ones:
+//   pack (src side in the fab):   chunk = [H.src(y) | hg | lg | L.src(y+1)]
+//   unpack (dst side in the fab): chunk = [hv | H.dst(y) | L.dst(y+1) | lv]
+// Returns H's index, or -1 when (a, b) is not such a pair.
+int seam_pair_hi(const ghx_exec *ex, int ia, int ib, bool pack) {
+  const DevTag &a = ex->htags[ia], &b = ex->htags[ib];
+  if (a.vlog != 4 || b.vlog != 4 || a.nxv != 1 || b.nxv != 1 || a.ny != b.ny || a.nz != b.nz || a.nvec != b.nvec ||
+      a.ny < 1)
+    return -1;
+  auto fits = [&](const DevTag &H, const DevTag &L) {
+    if (pack)
+      return H.src_ptr == L.src_ptr && H.src_sy == L.src_sy && H.src_sz == L.src_sz && H.src_sc == L.src_sc &&
+             L.src_off + L.src_sy == H.src_off + 3 && H.src_off % 2 == 0 && H.src_sy % 2 == 0 &&
+             H.src_sz % 2 == 0 && H.src_sc % 2 == 0;
+    return H.dst_ptr == L.dst_ptr && H.dst_sy == L.dst_sy && H.dst_sz == L.dst_sz && H.dst_sc == L.dst_sc &&
+           L.dst_off + L.dst_sy == H.dst_off + 1 && (H.dst_off - 1) % 2 == 0 && H.dst_sy % 2 == 0 &&
+           H.dst_sz % 2 == 0 && H.dst_sc % 2 == 0;
+  };
+  if (fits(a, b)) return ia;
+  if (fits(b, a)) return ib;
+  return -1;
+}
+
 // Order the sector-swap tags of one chain of fabs as an x-ring for
 // ring_task: T_j moves F_j's last sector <-> F_{j+1}'s first sector, every
 // fab appears once on each side, the ring closes, and for every fab the
@@ -1342,6 +1411,14 @@ std::vector<int32_t> ring_order(const ghx_exec *ex, const std::vector<int32_t> &
       return {};
   }
   return order;
+}
+
+bool seam_tasks_on() {  // GHX_SEAM_TASKS=0: host-memory remote x faces as plain pair copies
+  static const bool on = [] {
+    const char *v = std::getenv("GHX_SEAM_TASKS");
+    return !v || std::atoi(v) != 0;
+  }();
+  return on;
 }
 
 // Warp tasks.  Mirror tags (src<->dst swapped, opposite shift, same shape)
@@ -1421,6 +1498,7 @@ void build_tasks(ghx_exec *ex) {
   // sector fill: not over PCIe (ring executors: fabs in host memory, where
   // the extra 16-byte read costs a request)
   ex->nfill = 0;
+  ex->nseam = 0;
   auto fill_ok = [&](size_t i) { return !ex->ring && i < ex->hfill.size() && ex->hfill[i] && n < (1u << 30); };
   auto emit_bulk = [&](size_t i, std::vector<int4> &out) {
     const DevTag &t = ex->htags[i];
@@ -1448,6 +1526,21 @@ void build_tasks(ghx_exec *ex) {
         emit_bulk(i, out);
         emit_bulk(mate[i], out);
         continue;
+      }
+      // host-memory pack / unpack of a fab's remote x faces: seam tasks, one
+      // column of rows per task, one PCIe request per seam and side
+      if (ex->ring && ex->hremote[i] && ex->hremote[mate[i]] &&
+          (ex->kind == GHX_EXEC_PUSH_PACKED_ALL || ex->kind == GHX_EXEC_UNPACK_PACKED_ALL) && seam_tasks_on()) {
+        const bool pack = ex->kind == GHX_EXEC_PUSH_PACKED_ALL;
+        const int hi = seam_pair_hi(ex, (int)i, mate[i], pack);
+        if (hi >= 0) {
+          const int lo = hi == (int)i ? mate[i] : (int)i;
+          const DevTag &H = ex->htags[hi];
+          const uint32_t ncol = H.nvec / H.ny;
+          for (uint32_t q = 0; q < ncol; ++q) out.push_back(make_int4(hi, (int)q, pack ? -7 : -8, lo));
+          ex->nseam += 2;
+          continue;
+        }
       }
       if (fill_ok(i) && fill_ok(mate[i]) && ex->htags[mate[i]].nvec == nv) {
         ex->nfill += 2;
@@ -2282,11 +2375,11 @@ int launch(ghx_exec *ex, ghx_exec::Binding *bd, cudaStream_t st, const SyncArgs 
     SyncArgs plain = sync;
     plain.pe0 = plain.pe1 = 0;
     const int fb = std::max(blocks, face_blocks);
-    go(0, ex->pe0, blocks, ex->nring > 0, plain);
+    go(0, ex->pe0, blocks, ex->nring > 0 || ex->nseam > 0, plain);
     go(ex->pe0, ex->pe1 - ex->pe0, fb, false, plain);
     go(ex->pe1, ntasks - ex->pe1, fb, false, plain);
   } else {
-    go(0, ntasks, blocks, ex->nring > 0, sync);
+    go(0, ntasks, blocks, ex->nring > 0 || ex->nseam > 0, sync);  // seam tasks live in the ring instantiation
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "ghx_exec_run: launch");

@@ -41,6 +41,8 @@ def _worker(rank, world, port, q, seed0, env):
     try:
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
                           LOCAL_RANK="0")
+        env = dict(env)
+        memory = env.pop("_MEMORY", "device")
         os.environ.update(env)
         import torch
         import torch.distributed as dist
@@ -62,7 +64,7 @@ def _worker(rank, world, port, q, seed0, env):
             geom = amr.Geometry(dom, (0.0,) * 3, (1.0,) * 3, tuple(per))
             ba = amr.BoxArray([amr.Box(tuple(b[:3]), tuple(b[3:])) for b in boxes])
             ranks = [i % world for i in range(len(boxes))]
-            mf = amr.MultiFab(ba, amr.DistributionMapping(ranks, world), nc, amr.IntVect(*ng), geom)
+            mf = amr.MultiFab(ba, amr.DistributionMapping(ranks, world), nc, amr.IntVect(*ng), geom, memory=memory)
             mf.fill_hash(inputs.SEED, dom)
             torch.cuda.synchronize()
             for _ in range(2):
@@ -93,9 +95,11 @@ def _worker(rank, world, port, q, seed0, env):
 @pytest.mark.parametrize("env", [{}, {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "20"},
                                  {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "20", "GHX_REMOTE": "direct"},
                                  {"GHX_TRANSPORT": "nccl"}, {"GHX_SECTOR_FILL": "0"},
-                                 {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "20", "GHX_ONE_KERNEL": "0"}],
+                                 {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "20", "GHX_ONE_KERNEL": "0"},
+                                 {"_MEMORY": "pinned"}, {"_MEMORY": "pinned", "GHX_SEAM_TASKS": "0"},
+                                 {"_MEMORY": "pinned", "GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "20"}],
                          ids=["host-sync-packed", "devsync-packed", "devsync-direct", "fallback", "no-sector-fill",
-                              "devsync-two-kernels"])
+                              "devsync-two-kernels", "pinned", "pinned-no-seam-tasks", "pinned-devsync"])
 def test_random_layouts_across_processes(world, env):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()

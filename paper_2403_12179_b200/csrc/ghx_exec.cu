@@ -1220,7 +1220,6 @@ struct ghx_exec {
   // its last push task to that peer is done
   std::vector<int32_t> peer_total;
   int32_t *dpeer_total = nullptr;
-  int32_t nunpack = 0;  // EXCHANGE_PACKED: unpack tasks at the tail of htasks
   std::vector<int4> htasks;
   std::vector<int> hchain;  // chain tables (tag indices of consecutive seams)
   int *dchain = nullptr;
@@ -1751,7 +1750,6 @@ void build_tasks(ghx_exec *ex) {
   }
   // the unpacks last: every push and local task is grabbed before a warp
   // can wait on a peer's DONE
-  ex->nunpack = (int32_t)unp.size();
   a.insert(a.end(), unp.begin(), unp.end());
   ex->htasks.swap(a);
 }

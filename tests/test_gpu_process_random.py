@@ -37,7 +37,14 @@ def _layout(rng):
     return ext, boxes, ng, per
 
 
-def _worker(rank, world, port, q, seed0, env):
+def _fixed_layout(_rng):
+    """Two boxes of a periodic 16 x 8 x 8 domain: with 3 or 4 ranks, ranks 2
+    and 3 own no box and take part in the in-kernel protocol with empty
+    executors."""
+    return [16, 8, 8], np.asarray([[0, 0, 0, 7, 7, 7], [8, 0, 0, 15, 7, 7]], np.int64), [2, 1, 2], [True] * 3
+
+
+def _worker(rank, world, port, q, seed0, env, fixed=False):
     try:
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
                           LOCAL_RANK="0")
@@ -53,9 +60,9 @@ def _worker(rank, world, port, q, seed0, env):
         from oracle import ghost_oracle as go
         from oracle import inputs
         bad = []
-        for k in range(NLAYOUTS):
+        for k in range(1 if fixed else NLAYOUTS):
             rng = np.random.default_rng(seed0 + k)
-            ext, boxes, ng, per = _layout(rng)
+            ext, boxes, ng, per = (_fixed_layout if fixed else _layout)(rng)
             nc = int(rng.integers(1, 4))
             dt = np.float32 if k % 3 == 2 else np.float64
             amr.config.set_spacedim(3)
@@ -109,6 +116,25 @@ def test_random_layouts_across_processes(world, env):
     for p in procs:
         p.start()
     res = dict(q.get(timeout=900) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+    errs = [res[r] for r in range(world) if isinstance(res[r], str)]
+    assert not errs, "\n".join(e[-1500:] for e in errs)
+    assert all(res[r] == [] for r in range(world)), res
+
+
+@pytest.mark.parametrize("world", [3, 4])
+@pytest.mark.parametrize("env", [{"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "20"},
+                                 {"GHX_SYNC": "device", "GHX_BARRIER_TIMEOUT_S": "20", "GHX_ONE_KERNEL": "0"}, {}],
+                         ids=["devsync-one-kernel", "devsync-two-kernels", "host-sync"])
+def test_ranks_without_boxes(world, env):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, 0, env, True)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in range(world))
     for p in procs:
         p.join(timeout=120)
     errs = [res[r] for r in range(world) if isinstance(res[r], str)]

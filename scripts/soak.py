@@ -4,6 +4,7 @@ mode, then the wrapped-hash check -- looks for rare hangs or races in the
 rank synchronisation.  Usage:
     python scripts/soak.py [calls]
     torchrun --nproc-per-node 4 scripts/soak.py [calls]   (GHX_BENCH_BACKEND-style gloo)
+SOAK_MEMORY=pinned puts the fabs in pinned host memory.
 """
 import os
 import sys
@@ -26,7 +27,7 @@ ba = amr.decompose(dom, 16)
 
 def program(ctx):
     dm = amr.DistributionMapping.round_robin(len(ba), ctx.nranks)
-    mf = amr.MultiFab(ba, dm, 2, 2, geom)
+    mf = amr.MultiFab(ba, dm, 2, 2, geom, memory=os.environ.get("SOAK_MEMORY", "device"))
     mf.fill_hash(inputs.SEED, dom)
     torch.cuda.synchronize()
     for _ in range(CALLS):
@@ -34,7 +35,8 @@ def program(ctx):
     bad = 0
     for gi in mf.local_indices:
         f = mf.fabs[gi]
-        bad += int((device_bits(f) != expected_wrapped(f, 2, dom.as_row(), (1, 1, 1), inputs.SEED, 8)).sum())
+        exp = expected_wrapped(f, 2, dom.as_row(), (1, 1, 1), inputs.SEED, 8)
+        bad += int((device_bits(f).to(exp.device) != exp).sum())  # (pinned fabs: a host view)
     return bad
 
 
@@ -47,8 +49,8 @@ if "RANK" in os.environ:
     t = torch.tensor([bad])
     dist.all_reduce(t)
     if dist.get_rank() == 0:
-        print(f"process mode x{dist.get_world_size()}: {CALLS} calls in {time.perf_counter() - t0:.1f} s, "
-              f"{int(t.item())} bad cells")
+        print(f"process mode x{dist.get_world_size()} ({os.environ.get('SOAK_MEMORY', 'device')}): {CALLS} calls "
+              f"in {time.perf_counter() - t0:.1f} s, {int(t.item())} bad cells")
     dist.destroy_process_group()
 else:
     t0 = time.perf_counter()

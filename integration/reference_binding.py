@@ -487,7 +487,8 @@ class _AverageDown:
         self.ratio = np.array([int(ratio)] * d + [1] * (3 - d), np.int32)
         self.dim, self.ncomp = d, fine.ncomp
         self.item = next(iter(fine.fabs.values())).data.dtype.itemsize if fine.fabs else 8
-        assert rconfig.spacedim == d
+        if rconfig.spacedim != d:
+            raise ValueError(f"MultiFab has {d} axes, the reference is configured for {rconfig.spacedim}")
 
     def run(self) -> None:
         if len(self.jobs):

@@ -2393,6 +2393,10 @@ int ghx_exec_run(ghx_exec *ex, void *const *ptrs, int64_t nptrs, void *stream) {
     set_error("ghx_exec_run: pointer table must have nsrc + ndst + 2*nranks entries");
     return GHX_EINVAL;
   }
+  if (ex->kind == GHX_EXEC_EXCHANGE_PACKED) {  // its unpacks must wait for the peers' DONE
+    set_error("ghx_exec_run: GHX_EXEC_EXCHANGE_PACKED executors run through ghx_exec_run_synced only");
+    return GHX_EINVAL;
+  }
   if (ex->htasks.empty()) return GHX_OK;
   std::lock_guard<std::mutex> lk(ex->mu);
   DeviceGuard g(ex->device);
@@ -2433,6 +2437,10 @@ int ghx_exec_bind(ghx_exec *ex, void *const *ptrs, int64_t nptrs, void *stream, 
 int ghx_exec_run_bound(ghx_exec *ex, int64_t binding, void *stream) {
   if (!ex) {
     set_error("ghx_exec_run_bound: null handle");
+    return GHX_EINVAL;
+  }
+  if (ex->kind == GHX_EXEC_EXCHANGE_PACKED) {
+    set_error("ghx_exec_run_bound: GHX_EXEC_EXCHANGE_PACKED executors run through ghx_exec_run_synced only");
     return GHX_EINVAL;
   }
   if (ex->htasks.empty()) return GHX_OK;

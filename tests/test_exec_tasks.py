@@ -243,3 +243,23 @@ def test_exchange_packed_combines_push_and_unpack():
         assert np.array_equal(sx, sp) and np.array_equal(rx, ru) and rx.sum() > 0
     finally:
         N.lib.ghx_plan_free(h)
+
+
+def test_exchange_packed_runs_only_synced():
+    boxes = gu.scale_boxes(64, 16)
+    h = native_fb(boxes, [2] * 3, [1, 1, 1], [64] * 3, [i % 2 for i in range(len(boxes))], 2)
+    storage = boxes.copy()
+    storage[:, :3] -= 2
+    storage[:, 3:] += 2
+    storage = np.ascontiguousarray(storage)
+    ex = C.c_void_p()
+    try:
+        N.check(N.lib.ghx_exec_create(h, 0, N.EXEC_EXCHANGE_PACKED, N.i64p(storage), 2, N.i64p(storage), 2, 0, 0, 2,
+                                      8, 0, C.byref(ex)))
+        table = np.zeros(2 * len(boxes) + 4, np.uint64)
+        rc = N.lib.ghx_exec_run(ex, table.ctypes.data_as(C.POINTER(C.c_void_p)), len(table), None)
+        assert rc == 1 and b"run_synced" in N.lib.ghx_last_error()
+    finally:
+        if ex:
+            N.lib.ghx_exec_free(ex)
+        N.lib.ghx_plan_free(h)

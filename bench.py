@@ -626,6 +626,7 @@ def run_ours(args, cfg, rank, world):
                 x.run()
             ev1[i].record(stream)
         torch.cuda.synchronize()
+    launches = N.lib.ghx_launch_count() - l0  # the timed region only (not the diagnostic steps below)
     if x.mode == "process" and x.sync == "device":
         from paper_2403_12179_b200 import comm as _comm
         _comm.check_barriers()
@@ -655,7 +656,6 @@ def run_ours(args, cfg, rank, world):
                      "note": "median per rank, max over ranks; push includes the READY waits"
                              + ("; one kernel: push_kernel_ms is the whole exchange (pushes, local tags and "
                                 "unpacks in one launch)" if getattr(x, "one_kernel", False) else "")}
-    launches = N.lib.ghx_launch_count() - l0
     if dist:
         dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]

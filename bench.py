@@ -994,7 +994,7 @@ def e2e_binding_leg(cfg, L, mf, ghost_bytes, steps):
             "steps": steps, "first_call_s": round(first, 3), "verified": ok,
             "path": "integration/reference_binding.fill_boundary_native on the reference's own MultiFab "
                     "(miniamr_core, numpy fabs in pinned mapped memory via PinnedArena): ctypes -> libghostx.so "
-                    "(phased exchange, tile-ring seams, 8-CTA grid), every fab equal to the device run's"}
+                    "(phased exchange, tile-ring seams, 6-CTA grid), every fab equal to the device run's"}
 
 
 def main():

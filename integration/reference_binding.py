@@ -267,7 +267,7 @@ class _Prepared:
         _check(L.ghx_exec_create(self.plan, rank, kind, _p64(src.rows), src.ncomp, _p64(dst.rows), dst.ncomp, scomp,
                                  dcomp, ncomp, item, 0, C.byref(self.ex)))
         _check(L.ghx_exec_set_ring(self.ex, 1))
-        _check(L.ghx_exec_set_grid(self.ex, 8, 256))
+        _check(L.ghx_exec_set_grid(self.ex, 6, 256))
         ns, nd = len(src.rows), len(dst.rows)
         self.table = np.zeros(ns + nd + 2 * nranks, np.uint64)  # [src fabs][dst fabs][send][recv]
         for i, a in src.addrs.items():

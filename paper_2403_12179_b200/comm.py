@@ -489,8 +489,10 @@ class Executor:
         if host:
             # fabs in host memory: the PCIe / IOMMU path saturates with few
             # concurrent warps and degrades with many (scattered 32-64 B
-            # requests); 8 CTAs measured best (C2 e2e 9.6 -> 7.4 ms)
-            N.check(N.lib.ghx_exec_set_grid(h, int(os.environ.get("GHX_HOST_BLOCKS", "8")), 256))
+            # requests); 6 CTAs measured best with the phased exchange and
+            # tile-ring seams (C3 e2e 49.4 -> 47.9 ms, C4 28.0 -> 26.8; C2
+            # 5.76 -> 5.87; 4, 5, 7, 10, 12, 16 slower)
+            N.check(N.lib.ghx_exec_set_grid(h, int(os.environ.get("GHX_HOST_BLOCKS", "6")), 256))
         self.plan = plan
         self.device = device
         self.nsrc = len(src_rows)
